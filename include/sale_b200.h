@@ -1,0 +1,161 @@
+/*
+ * sale_b200.h — C ABI of the B200-native SALE prefill path (sm_100a).
+ *
+ * The drop-in boundary for the reference's hot path (the header-only
+ * `namespace sale` in /root/reference/proj/include/sale). Every entry point
+ * names the reference function it replaces (file:line). Plain pointers and
+ * sizes only; no torch / C++ types. All status codes are int:
+ *
+ *   0  SALE_B200_OK
+ *   1  SALE_B200_INVALID_ARGUMENT   (reference throws std::invalid_argument)
+ *   2  SALE_B200_DOMAIN_ERROR       (reference throws std::domain_error)
+ *   3  SALE_B200_OUT_OF_RANGE       (reference throws std::out_of_range)
+ *   4  SALE_B200_CUDA_ERROR
+ *   5  SALE_B200_UNSUPPORTED        (valid for the reference, not on this path:
+ *                                    see DESIGN.md "Scope")
+ *
+ * Device data layout (all device pointers, caller-allocated):
+ *   q            bf16 [B][N][Hq][128]      rows padded with zeros past head_dim
+ *   k, v         bf16 [B][N][Hkv][128]
+ *   q_codes      int8 [B][N][Hq][128]      4-bit codes in [-7, 7]
+ *   k_codes      int8 [B][N][Hkv][128]
+ *   q_scales     f32  [B][Hq][N]           one per token        (quant.hpp:95-104)
+ *   k_scales     f32  [B][Hkv][ceil(N/32)] one per key block    (quant.hpp:107-119)
+ *   mask_words   u32  [B][Hq][ceil(N/64)][ceil(ceil(N/32)/32)] packed BlockMask
+ *                (bit j%32 of word j/32 of row i == BlockMask::get(i, j))
+ *   out          bf16 [B][N][Hq][128]
+ * Geometry: the reference's default SelectionConfig (selection.hpp:18-24):
+ * block_q 64, block_k 32, segment 4, sink 32 tokens, local >= 128 tokens; Hq a
+ * multiple of Hkv (GQA); head_dim <= 128 (the row pitch is always 128).
+ *
+ * Streams: every call is stream-ordered and asynchronous unless it says
+ * otherwise; `stream` is a cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef SALE_B200_H
+#define SALE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SALE_B200_OK 0
+#define SALE_B200_INVALID_ARGUMENT 1
+#define SALE_B200_DOMAIN_ERROR 2
+#define SALE_B200_OUT_OF_RANGE 3
+#define SALE_B200_CUDA_ERROR 4
+#define SALE_B200_UNSUPPORTED 5
+
+typedef struct sale_b200_ctx sale_b200_ctx;
+
+/* Mirrors sale::SelectionConfig (selection.hpp:18-38) minus the per-head tau. */
+typedef struct {
+    int64_t sink_tokens;      /* 32  */
+    int64_t local_tokens_min; /* 128 */
+    int64_t segment_size;     /* 4   */
+    int64_t block_q;          /* 64  */
+    int64_t block_k;          /* 32  */
+} sale_b200_selection_config;
+
+/* Problem shape shared by the stage entry points. head_dim is the logical d
+ * (1..128) used for 1/sqrt(d); storage rows are always 128 wide. */
+typedef struct {
+    int64_t batch;
+    int64_t tokens;
+    int64_t q_heads;
+    int64_t kv_heads;
+    int64_t head_dim;
+} sale_b200_shape;
+
+/* Optional parity outputs of the Selection-Pass (any pointer may be NULL).
+ * running_max / exp_sum / bound: f64 [B][Hq][N] for query blocks with a
+ * non-empty middle region (selection.hpp:246-251), untouched elsewhere.
+ * block_max: int32 [B][Hq][N][ceil(N/32)], the per-row integer maximum of every
+ * estimated middle block (quant.hpp:170-179), untouched elsewhere. */
+typedef struct {
+    double *running_max;
+    double *exp_sum;
+    double *bound;
+    int32_t *block_max;
+} sale_b200_select_debug;
+
+/* ---- context ------------------------------------------------------------ */
+int sale_b200_ctx_create(int device, sale_b200_ctx **out);
+void sale_b200_ctx_destroy(sale_b200_ctx *ctx);
+/* Message of the last failing call on ctx (or of ctx creation when ctx==NULL). */
+const char *sale_b200_last_error(const sale_b200_ctx *ctx);
+int sale_b200_version(void);
+void sale_b200_default_config(sale_b200_selection_config *cfg);
+
+/* ---- stage 1: quantization ----------------------------------------------
+ * Replaces quantize_per_token (quant.hpp:95) when group_rows == 1 and
+ * quantize_per_key_block (quant.hpp:107) when group_rows == 32, for every
+ * (batch, head) of x [B][N][H][128] in one launch. */
+int sale_b200_quantize(sale_b200_ctx *ctx, const void *x, int64_t batch, int64_t tokens,
+                       int64_t heads, int64_t group_rows, int8_t *codes, float *scales,
+                       void *stream);
+/* Fused Q (per token) + K (per key block) quantization in ONE launch. */
+int sale_b200_quantize_qk(sale_b200_ctx *ctx, const void *q, const void *k,
+                          const sale_b200_shape *shape, int8_t *q_codes, float *q_scales,
+                          int8_t *k_codes, float *k_scales, void *stream);
+
+/* ---- stage 2: Selection-Pass --------------------------------------------
+ * Replaces selection_pass (selection.hpp:211) for every (batch, q head):
+ * sink_local_index_set (:92) + compute_sink_local_stats (:129) +
+ * threshold_bound (:168) + approx_weight_block / max_then_dequantize
+ * (quant.hpp:136-179) + segment_aggregate (:182). taus: HOST array of q_heads
+ * doubles (per-head tau, runner.hpp:59-60). */
+int sale_b200_select(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *q_codes,
+                     const float *q_scales, const int8_t *k_codes, const float *k_scales,
+                     const sale_b200_shape *shape, const double *taus,
+                     const sale_b200_selection_config *cfg, uint32_t *mask_words,
+                     const sale_b200_select_debug *dbg, void *stream);
+
+/* ---- stage 3: Computation-Pass ------------------------------------------
+ * Replaces block_sparse_attention (sparse_attention.hpp:37); with
+ * mask_words == NULL it is the all-true mask, i.e. full_attention
+ * (attention.hpp:18). coverage (optional): int32 [B][Hq][N] attended tokens per
+ * row (SparseAttentionOutput::coverage). */
+int sale_b200_sparse_attention(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                               const sale_b200_shape *shape, const uint32_t *mask_words,
+                               void *out, int32_t *coverage, void *stream);
+
+/* ---- accounting ----------------------------------------------------------
+ * Replaces flop_accounting (sparse_attention.hpp:101): counts (device int64
+ * [B][Hq][3]) = computed, skipped, total causal blocks per head. */
+int sale_b200_flop_count(sale_b200_ctx *ctx, const uint32_t *mask_words, int64_t batch,
+                         int64_t q_heads, int64_t tokens, int64_t *counts, void *stream);
+
+/* ---- whole prefill --------------------------------------------------------
+ * The run_pipeline stage composition (runner.hpp:63-80) on device buffers:
+ * quantize -> select -> sparse attention, with codes / scales / thresholds /
+ * mask in ctx-owned workspace. mask_out (optional, device) receives the mask. */
+int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                      const sale_b200_shape *shape, const double *taus,
+                      const sale_b200_selection_config *cfg, void *out, uint32_t *mask_out,
+                      void *stream);
+/* Same, end to end from HOST buffers (bf16 bit patterns, uint16): H2D copies,
+ * the three stages and the D2H copy of out, synchronous on return. */
+int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t *k,
+                           const uint16_t *v, const sale_b200_shape *shape, const double *taus,
+                           const sale_b200_selection_config *cfg, uint16_t *out);
+
+/* ---- synthetic workload (host, not the hot path) --------------------------
+ * workloads.hpp:125-159 sink_local_head / :104-112 gaussian_head for one head
+ * (kind 0 gaussian, 1 sink_local), fp32 [n][d] each, bit-identical to the
+ * reference generator. */
+int sale_b200_workload_head_f32(int kind, uint64_t seed, int64_t n, int64_t d, int64_t head,
+                                float *q, float *k, float *v);
+/* GQA extension written as bf16 [B][N][H][128] host arrays
+ * (rows zero-padded past d): KV head g of batch b is the reference head g of
+ * seed+b; query head r>0 of the group adds fresh N(0,1) noise to the same
+ * planted terms. threads <= 0 means all cores. */
+int sale_b200_workload_gqa_bf16(int kind, uint64_t seed, const sale_b200_shape *shape,
+                                uint16_t *q, uint16_t *k, uint16_t *v, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SALE_B200_H */

@@ -1,0 +1,389 @@
+// attention.cu — K3: block-sparse causal flash attention on tcgen05 (bf16 in,
+// fp32 TMEM accumulators, fp32 online softmax) that visits only selected
+// 64x32 blocks. With mask == nullptr it is the dense causal baseline (the
+// all-ones-mask run of the same kernel).
+//
+// Replaces block_sparse_attention (sparse_attention.hpp:37-97) and, as the
+// dense run, full_attention (attention.hpp:18-50). Semantics kept: a key token
+// t contributes to row g iff t <= g and mask(qblock(g), kblock(t)) is set;
+// fully-future mask bits are ignored; coverage[g] counts the attended tokens.
+//
+// CTA = one (batch, head) x 128-row query tile = query blocks (2t-1, 2t), rows
+// [128t-64, 128t+64). Key tiles follow the segment grid of the Selection-Pass:
+// tile 0 = the 32-key sink block, tile s+1 = keys [32+128s, 160+128s) = key
+// blocks 1+4s..4+4s. A tile is visited iff any of its 8 (qblock, kblock) bits is
+// set; inside a visited tile unselected 32-key sub-blocks and the causal
+// diagonal are masked per row.
+//
+// Pipeline (warp-specialised, one elected thread per role):
+//   warp 0  TMA: Q once, then K_j, V_j into a 2-stage ring (SW128 tiles)
+//   warp 1  MMA: S_j = Q K_j^T into TMEM buffer j%2 (8 x K=16), then
+//           O += P_{j-1} V_{j-1} with P read straight from TMEM (A operand)
+//   warps 4-7  softmax, thread = row: tcgen05.ld S row, mask, lazy-rescaled
+//           online softmax in the exp2 domain (O rescaled in TMEM only when
+//           the running max grows by > 8), P -> bf16 -> tcgen05.st over S.
+#include "common.cuh"
+
+namespace sale_b200 {
+
+constexpr int kAttnThreads = 256;
+constexpr int kMaxTiles = 4200;           // supports N <= 512K
+constexpr int kTileBytesHalf = 128 * 64 * 2;   // 128 rows x 64 bf16 = 16 KB
+constexpr uint32_t kColO = 0, kColS0 = 128;    // TMEM: O | S0 | S1
+
+struct AttnSmem {
+    alignas(1024) uint8_t q[2][kTileBytesHalf];
+    alignas(1024) uint8_t k[2][2][kTileBytesHalf];
+    alignas(1024) uint8_t v[2][2][kTileBytesHalf];
+    uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full[2], pv_done[2];
+    uint32_t tmem_base;
+    int ntiles;
+    int warp_cnt[8];
+    uint32_t tiles[kMaxTiles]; // j | bits8 << 16
+};
+
+namespace {
+
+__device__ __forceinline__ uint32_t mask_bits4(const uint32_t *row, int64_t words, int64_t j0) {
+    // bits j0 .. j0+3 of a packed mask row
+    const int64_t w = j0 >> 5;
+    const int sh = static_cast<int>(j0 & 31);
+    uint64_t v = row[w];
+    if (w + 1 < words) v |= static_cast<uint64_t>(row[w + 1]) << 32;
+    return static_cast<uint32_t>(v >> sh) & 0xFu;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&p);
+}
+
+struct SoftmaxState {
+    float m_run = -INFINITY; // running max, exp2 domain (logit * scale_log2)
+    float l_run = 0.0f;      // running sum of p
+    int cov = 0;             // attended tokens
+};
+
+// One S tile of one row (thread): mask, lazy online-softmax update, P -> TMEM.
+// NK = keys in the tile (32 for the sink tile, 128 otherwise). S holds raw
+// fp32 logits*sqrt(d) bits; P (bf16 pairs) is written over the first NK/2
+// columns of the same buffer.
+template <int NK>
+__device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uint32_t nib,
+                                             int64_t lim, float scale_log2, SoftmaxState &st,
+                                             uint64_t *pv_prev, uint32_t pv_parity) {
+    uint32_t s[NK];
+#pragma unroll
+    for (int c4 = 0; c4 < NK / 32; ++c4)
+        tmem_ld32(sAddr + 32 * c4, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c4]));
+    tmem_ld_wait();
+    // column c valid iff its 32-key sub-block is selected and c <= lim (causal)
+    float mt = -INFINITY;
+    int nvalid = 0;
+#pragma unroll
+    for (int c = 0; c < NK; ++c) {
+        const bool ok = ((nib >> (c >> 5)) & 1u) && c <= lim;
+        const float v = ok ? __uint_as_float(s[c]) : -INFINITY;
+        s[c] = __float_as_uint(v);
+        mt = fmaxf(mt, v);
+        nvalid += ok ? 1 : 0;
+    }
+    const float m_new = fmaxf(st.m_run, mt * scale_log2);
+    const bool need = st.m_run != -INFINITY && m_new > st.m_run + 8.0f;
+    if (st.m_run == -INFINITY) st.m_run = m_new;
+    if (__any_sync(0xffffffffu, need)) {
+        // O must hold PV of every earlier tile before it is rescaled
+        mbar_wait(pv_prev, pv_parity);
+        tc_fence_after();
+        const float alpha = need ? ex2_approx(st.m_run - m_new) : 1.0f;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(oAddr + 32 * cc, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(oAddr + 32 * cc, o);
+        }
+        tmem_st_wait();
+        if (need) {
+            st.l_run *= alpha;
+            st.m_run = m_new;
+        }
+    }
+    const float neg_m = -st.m_run;
+    float psum = 0.0f;
+#pragma unroll
+    for (int c2 = 0; c2 < NK / 2; ++c2) {
+        const float x0 = __uint_as_float(s[2 * c2]), x1 = __uint_as_float(s[2 * c2 + 1]);
+        const float p0 = x0 == -INFINITY ? 0.0f : ex2_approx(fmaf(x0, scale_log2, neg_m));
+        const float p1 = x1 == -INFINITY ? 0.0f : ex2_approx(fmaf(x1, scale_log2, neg_m));
+        psum += p0 + p1;
+        s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
+    }
+    st.l_run += psum;
+    st.cov += nvalid;
+    if constexpr (NK == 128) {
+        tmem_st32(sAddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_st32(sAddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+    } else {
+        tmem_st16(sAddr, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
+    }
+    tmem_st_wait();
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
+sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const uint32_t *__restrict__ mask,
+                        __nv_bfloat16 *__restrict__ out, int32_t *__restrict__ coverage,
+                        int64_t tokens, int hq, int hkv, int batch, float scale_log2) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    AttnSmem &sm = *reinterpret_cast<AttnSmem *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int tid = threadIdx.x;
+
+    const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
+    const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
+    const int64_t words = (nk + 31) / 32;
+    const int n_t = static_cast<int>(nq / 2 + 1);
+    const int bh = batch * hq;
+    const int t = n_t - 1 - static_cast<int>(blockIdx.x / bh); // heaviest tiles first
+    const int rest = static_cast<int>(blockIdx.x % bh);
+    const int h = rest % hq;
+    const int b = rest / hq;
+    const int g = h / (hq / hkv);
+    const int row0 = 128 * t - 64;
+    const int64_t qa = 2 * static_cast<int64_t>(t) - 1, qb = 2 * static_cast<int64_t>(t);
+
+    if (tid == 0) {
+        mbar_init(&sm.q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.k_full[s], 1);
+            mbar_init(&sm.v_full[s], 1);
+            mbar_init(&sm.kv_empty[s], 1);
+            mbar_init(&sm.s_full[s], 1);
+            mbar_init(&sm.p_full[s], 4);
+            mbar_init(&sm.pv_done[s], 1);
+        }
+        sm.ntiles = 0;
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+
+    // ---- active tile list (block-wide stream compaction, ascending order)
+    const uint32_t *rowA = (mask && qa >= 0) ? mask + ((static_cast<int64_t>(b) * hq + h) * nq + qa) * words : nullptr;
+    const uint32_t *rowB = (mask && qb < nq) ? mask + ((static_cast<int64_t>(b) * hq + h) * nq + qb) * words : nullptr;
+    const int total = t + 2;
+    __syncthreads();
+    for (int start = 0; start < total; start += kAttnThreads) {
+        const int j = start + tid;
+        uint32_t bits = 0;
+        if (j < total) {
+            const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
+            if (key0 < tokens) {
+                const int64_t j0 = j == 0 ? 0 : 1 + 4LL * (j - 1);
+                const int nsub = j == 0 ? 1 : 4;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int64_t qi = half == 0 ? qa : qb;
+                    if (qi < 0 || qi >= nq) continue;
+                    const uint32_t *row = half == 0 ? rowA : rowB;
+                    uint32_t nib = mask ? mask_bits4(row, words, j0) : 0xFu;
+                    nib &= (1u << nsub) - 1u;
+                    // drop fully-future and out-of-range key blocks
+                    for (int e = 0; e < nsub; ++e) {
+                        const int64_t jb = j0 + e;
+                        if (jb >= nk || jb * kBlockK >= (qi + 1) * kBlockQ) nib &= ~(1u << e);
+                    }
+                    bits |= nib << (4 * half);
+                }
+            }
+        }
+        const bool active = bits != 0;
+        const uint32_t ballot = __ballot_sync(0xffffffffu, active);
+        if (lane == 0) sm.warp_cnt[warp] = __popc(ballot);
+        __syncthreads();
+        int base = sm.ntiles;
+        for (int w = 0; w < warp; ++w) base += sm.warp_cnt[w];
+        if (active) {
+            const int pos = base + __popc(ballot & ((1u << lane) - 1u));
+            if (pos < kMaxTiles) sm.tiles[pos] = static_cast<uint32_t>(j) | (bits << 16);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int s = sm.ntiles;
+            for (int w = 0; w < kAttnThreads / 32; ++w) s += sm.warp_cnt[w];
+            sm.ntiles = s < kMaxTiles ? s : kMaxTiles;
+        }
+        __syncthreads();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+    const int ntiles = sm.ntiles;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA
+        if (elect_one() && ntiles > 0) {
+            tma_prefetch(&tm_q);
+            tma_prefetch(&tm_k);
+            tma_prefetch(&tm_v);
+            mbar_expect_tx(&sm.q_full, 2 * kTileBytesHalf);
+            tma_load_4d(sm.q[0], &tm_q, &sm.q_full, 0, h, row0, b);
+            tma_load_4d(sm.q[1], &tm_q, &sm.q_full, 64, h, row0, b);
+            for (int jj = 0; jj < ntiles; ++jj) {
+                const int st = jj & 1;
+                const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
+                const int key0 = j == 0 ? 0 : kBlockK + 128 * (j - 1);
+                mbar_wait(&sm.kv_empty[st], ((jj >> 1) & 1) ^ 1);
+                mbar_expect_tx(&sm.k_full[st], 2 * kTileBytesHalf);
+                tma_load_4d(sm.k[st][0], &tm_k, &sm.k_full[st], 0, g, key0, b);
+                tma_load_4d(sm.k[st][1], &tm_k, &sm.k_full[st], 64, g, key0, b);
+                mbar_expect_tx(&sm.v_full[st], 2 * kTileBytesHalf);
+                tma_load_4d(sm.v[st][0], &tm_v, &sm.v_full[st], 0, g, key0, b);
+                tma_load_4d(sm.v[st][1], &tm_v, &sm.v_full[st], 64, g, key0, b);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA
+        if (elect_one() && ntiles > 0) {
+            constexpr uint32_t idesc_pv = idesc_bf16(128, 128, true);
+            const uint64_t qdesc0 = umma_desc_sw128(smem_u32(sm.q[0]), 16, 1024);
+            const uint64_t qdesc1 = umma_desc_sw128(smem_u32(sm.q[1]), 16, 1024);
+            mbar_wait(&sm.q_full, 0);
+            tc_fence_after();
+            for (int jj = 0; jj <= ntiles; ++jj) {
+                if (jj < ntiles) {
+                    const int st = jj & 1;
+                    const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
+                    const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
+                    mbar_wait(&sm.k_full[st], (jj >> 1) & 1);
+                    tc_fence_after();
+                    const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
+                    const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
+                    const uint32_t dS = tmem + kColS0 + 128u * static_cast<uint32_t>(st);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint64_t a = (kk < 4 ? qdesc0 : qdesc1) + 2 * (kk & 3);
+                        const uint64_t bd = (kk < 4 ? kd0 : kd1) + 2 * (kk & 3);
+                        mma_bf16_ss(dS, a, bd, idesc_s, kk > 0);
+                    }
+                    tc_commit(&sm.s_full[st]);
+                }
+                if (jj > 0) {
+                    const int p = jj - 1;
+                    const int pst = p & 1;
+                    const int jp = static_cast<int>(sm.tiles[p] & 0xFFFFu);
+                    const int steps = jp == 0 ? 2 : 8;
+                    mbar_wait(&sm.p_full[pst], (p >> 1) & 1);
+                    mbar_wait(&sm.v_full[pst], (p >> 1) & 1);
+                    tc_fence_after();
+                    const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
+                    const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(pst);
+                    for (int kk = 0; kk < steps; ++kk)
+                        mma_bf16_ts(tmem + kColO, aP + 8 * kk, vd + 128 * kk, // +16 keys = 2 KB
+                                    idesc_pv, (p > 0 || kk > 0) ? 1u : 0u);
+                    tc_commit(&sm.kv_empty[pst]);
+                    tc_commit(&sm.pv_done[pst]);
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ softmax
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const int64_t grow = static_cast<int64_t>(row0) + r;
+        const bool row_ok = grow >= 0 && grow < tokens;
+        const int half = r >> 6;
+        const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        SoftmaxState st;
+        for (int jj = 0; jj < ntiles; ++jj) {
+            const int sb = jj & 1;
+            const uint32_t info = sm.tiles[jj];
+            const int j = static_cast<int>(info & 0xFFFFu);
+            const uint32_t nib = (info >> (16 + 4 * half)) & 0xFu;
+            const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
+            const int64_t lim = row_ok ? grow - key0 : -1; // valid columns c <= lim
+            const uint32_t sAddr = lane_addr + kColS0 + 128u * sb;
+            mbar_wait(&sm.s_full[sb], (jj >> 1) & 1);
+            tc_fence_after();
+            const int pj = jj - 1;
+            if (j == 0)
+                softmax_tile<32>(sAddr, lane_addr + kColO, nib, lim, scale_log2, st,
+                                 &sm.pv_done[pj & 1], (pj >> 1) & 1);
+            else
+                softmax_tile<128>(sAddr, lane_addr + kColO, nib, lim, scale_log2, st,
+                                  &sm.pv_done[pj & 1], (pj >> 1) & 1);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.p_full[sb]);
+        }
+        // ---- epilogue: O / l -> bf16
+        if (ntiles > 0) {
+            const int last = ntiles - 1;
+            mbar_wait(&sm.pv_done[last & 1], (last >> 1) & 1);
+            tc_fence_after();
+        }
+        const float inv_l = st.l_run > 0.0f ? 1.0f / st.l_run : 0.0f;
+        __nv_bfloat16 *dst = row_ok ? out + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim : nullptr;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            if (ntiles > 0) {
+                tmem_ld32(lane_addr + kColO + 32 * cc, o);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] = 0u;
+            }
+            if (row_ok) {
+                uint4 w[4];
+                uint32_t *wp = reinterpret_cast<uint32_t *>(w);
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    wp[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+                uint4 *d4 = reinterpret_cast<uint4 *>(dst + 32 * cc);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) d4[e] = w[e];
+            }
+        }
+        if (row_ok && coverage) coverage[(static_cast<int64_t>(b) * hq + h) * tokens + grow] = st.cov;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+} // namespace
+
+size_t attention_smem_bytes() { return sizeof(AttnSmem) + 1024; }
+
+cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &tm_k,
+                                    const CUtensorMap &tm_v, const uint32_t *mask, void *out,
+                                    int32_t *coverage, int64_t batch, int64_t tokens, int hq,
+                                    int hkv, float scale_log2, cudaStream_t stream) {
+    const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
+    if (nq / 2 + 1 > kMaxTiles - 2) return cudaErrorInvalidValue;
+    static bool configured = false;
+    const size_t smem = attention_smem_bytes();
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(sparse_attention_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int64_t grid = (nq / 2 + 1) * batch * hq;
+    sparse_attention_kernel<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
+        tm_q, tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out), coverage, tokens, hq, hkv,
+        static_cast<int>(batch), scale_log2);
+    return cudaGetLastError();
+}
+
+} // namespace sale_b200

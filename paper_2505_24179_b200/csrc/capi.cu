@@ -1,0 +1,473 @@
+// capi.cu — the C ABI (include/sale_b200.h): argument validation with the
+// reference's error classes, TMA tensor-map construction, work-unit tables,
+// ctx-owned workspace, and the stage composition of run_pipeline
+// (runner.hpp:63-80) on device buffers.
+#include "sale_b200.h"
+
+#include "common.cuh"
+#include "internal.h"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace sale_b200;
+
+struct sale_b200_ctx {
+    int device = 0;
+    std::string err;
+    std::mutex mu;
+    // workspace for sale_b200_select / sale_b200_prefill
+    uint8_t *ws = nullptr;
+    size_t ws_bytes = 0;
+    double *d_taus = nullptr;
+    int64_t taus_cap = 0;
+    // estimator work-unit table, cached per token count
+    EstUnit *d_units = nullptr;
+    int64_t units_cap = 0;
+    int64_t units_tokens = -1;
+    int64_t n_units = 0;
+    // host e2e buffers
+    uint8_t *io = nullptr;
+    size_t io_bytes = 0;
+    cudaStream_t io_stream = nullptr;
+};
+
+namespace {
+
+std::string g_create_error;
+
+int fail(sale_b200_ctx *ctx, int code, const std::string &msg) {
+    if (ctx) ctx->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+
+int cuda_fail(sale_b200_ctx *ctx, cudaError_t e, const char *where) {
+    return fail(ctx, SALE_B200_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define SALE_CUDA(ctx, call)                                                                       \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);                                   \
+    } while (0)
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int check_shape(sale_b200_ctx *ctx, const sale_b200_shape *s) {
+    if (!s) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "shape is NULL");
+    if (s->batch < 1 || s->tokens < 1 || s->q_heads < 1 || s->kv_heads < 1)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "HeadInput: empty query");
+    if (s->head_dim < 1) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "HeadInput: empty query");
+    if (s->head_dim > kHeadDim)
+        return fail(ctx, SALE_B200_UNSUPPORTED, "head_dim > 128 is not supported on the B200 path");
+    if (s->q_heads % s->kv_heads != 0)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "q_heads must be a multiple of kv_heads");
+    if (s->tokens > (1LL << 19))
+        return fail(ctx, SALE_B200_UNSUPPORTED, "tokens > 524288 is not supported");
+    if (s->batch * s->kv_heads > 65535)
+        return fail(ctx, SALE_B200_UNSUPPORTED, "batch * kv_heads > 65535");
+    return SALE_B200_OK;
+}
+
+// SelectionConfig::validate (selection.hpp:26-37), then the geometry this
+// path is specialised for.
+int check_config(sale_b200_ctx *ctx, const sale_b200_selection_config *c) {
+    sale_b200_selection_config d;
+    sale_b200_default_config(&d);
+    if (!c) c = &d;
+    if (c->sink_tokens < 1)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "SelectionConfig: sink_tokens must be >= 1");
+    if (c->block_q < 1 || c->block_k < 1)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "SelectionConfig: block sizes must be >= 1");
+    if (c->local_tokens_min < c->block_k)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT,
+                    "SelectionConfig: local_tokens_min must be >= block_k");
+    if (c->segment_size < 1)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "SelectionConfig: segment_size must be >= 1");
+    if (c->sink_tokens != d.sink_tokens || c->local_tokens_min != d.local_tokens_min ||
+        c->segment_size != d.segment_size || c->block_q != d.block_q || c->block_k != d.block_k)
+        return fail(ctx, SALE_B200_UNSUPPORTED,
+                    "the B200 path implements the default SelectionConfig geometry "
+                    "(block_q 64, block_k 32, segment 4, sink 32, local 128)");
+    return SALE_B200_OK;
+}
+
+int check_taus(sale_b200_ctx *ctx, const double *taus, int64_t n) {
+    if (!taus) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "taus is NULL");
+    for (int64_t i = 0; i < n; ++i)
+        if (!(taus[i] > 0.0 && taus[i] < 1.0))
+            return fail(ctx, SALE_B200_INVALID_ARGUMENT, "SelectionConfig: tau must be in (0,1)");
+    return SALE_B200_OK;
+}
+
+float inv_sqrt_dim(int64_t d) { return 1.0f / std::sqrt(static_cast<float>(d)); }
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 4-D map over [B][N][H][128] with a SWIZZLE_128B box of
+// {box_inner elements, 1 head, box_rows tokens, 1 batch}.
+int make_map(sale_b200_ctx *ctx, CUtensorMap *map, const void *base, bool bf16, int64_t batch,
+             int64_t tokens, int64_t heads, uint32_t box_inner, uint32_t box_rows) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return fail(ctx, SALE_B200_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const uint64_t eb = bf16 ? 2 : 1;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(kHeadDim), static_cast<cuuint64_t>(heads),
+                          static_cast<cuuint64_t>(tokens), static_cast<cuuint64_t>(batch)};
+    cuuint64_t strides[3] = {kHeadDim * eb, static_cast<cuuint64_t>(heads) * kHeadDim * eb,
+                             static_cast<cuuint64_t>(tokens * heads) * kHeadDim * eb};
+    cuuint32_t box[4] = {box_inner, 1, box_rows, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 4,
+                     const_cast<void *>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(ctx, SALE_B200_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return SALE_B200_OK;
+}
+
+// Work units of the estimator (estimate.cu): every 128-row tile m >= 2 with
+// q-block 2m+1 present, split into chunks of 16 middle segments. Full chunks
+// first (by chunk, then tile: concurrent CTAs share K-code chunks in L2),
+// partial chunks last, largest first.
+int ensure_units(sale_b200_ctx *ctx, int64_t tokens, cudaStream_t stream) {
+    if (ctx->units_tokens == tokens) return SALE_B200_OK;
+    const int64_t nq = cdiv(tokens, kBlockQ);
+    std::vector<EstUnit> units;
+    for (int64_t m = 2; 2 * m + 1 <= nq - 1; ++m) {
+        const int64_t f = m - 1;
+        for (int64_t c = 0; c * kSegPerUnitHost < f; ++c)
+            units.push_back({static_cast<int>(m), static_cast<int>(c),
+                             static_cast<int>(std::min<int64_t>(kSegPerUnitHost, f - c * kSegPerUnitHost))});
+    }
+    std::stable_sort(units.begin(), units.end(), [](const EstUnit &a, const EstUnit &b) {
+        if (a.nseg != b.nseg) return a.nseg > b.nseg;
+        if (a.c != b.c) return a.c < b.c;
+        return a.m < b.m;
+    });
+    const int64_t n = static_cast<int64_t>(units.size());
+    if (n > ctx->units_cap) {
+        if (ctx->d_units) cudaFree(ctx->d_units);
+        ctx->d_units = nullptr;
+        SALE_CUDA(ctx, cudaMalloc(&ctx->d_units, sizeof(EstUnit) * std::max<int64_t>(n, 1)));
+        ctx->units_cap = std::max<int64_t>(n, 1);
+    }
+    if (n)
+        SALE_CUDA(ctx, cudaMemcpyAsync(ctx->d_units, units.data(), sizeof(EstUnit) * n,
+                                       cudaMemcpyHostToDevice, stream));
+    SALE_CUDA(ctx, cudaStreamSynchronize(stream));
+    ctx->units_tokens = tokens;
+    ctx->n_units = n;
+    return SALE_B200_OK;
+}
+
+struct Workspace {
+    int8_t *q_codes;
+    int8_t *k_codes;
+    float *q_scales;
+    float *k_scales;
+    float *thresh;
+    uint32_t *mask;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+int ensure_workspace(sale_b200_ctx *ctx, const sale_b200_shape &s, Workspace *w) {
+    const int64_t B = s.batch, N = s.tokens, Hq = s.q_heads, Hkv = s.kv_heads;
+    const int64_t nq = cdiv(N, kBlockQ), nk = cdiv(N, kBlockK), words = cdiv(nk, 32);
+    const size_t sz[6] = {align256(B * N * Hq * kHeadDim), align256(B * N * Hkv * kHeadDim),
+                          align256(sizeof(float) * B * Hq * N), align256(sizeof(float) * B * Hkv * nk),
+                          align256(sizeof(float) * B * Hq * N),
+                          align256(sizeof(uint32_t) * B * Hq * nq * words)};
+    size_t total = 0;
+    for (size_t x : sz) total += x;
+    if (total > ctx->ws_bytes) {
+        if (ctx->ws) cudaFree(ctx->ws);
+        ctx->ws = nullptr;
+        ctx->ws_bytes = 0;
+        SALE_CUDA(ctx, cudaMalloc(&ctx->ws, total));
+        ctx->ws_bytes = total;
+    }
+    uint8_t *p = ctx->ws;
+    w->q_codes = reinterpret_cast<int8_t *>(p);
+    p += sz[0];
+    w->k_codes = reinterpret_cast<int8_t *>(p);
+    p += sz[1];
+    w->q_scales = reinterpret_cast<float *>(p);
+    p += sz[2];
+    w->k_scales = reinterpret_cast<float *>(p);
+    p += sz[3];
+    w->thresh = reinterpret_cast<float *>(p);
+    p += sz[4];
+    w->mask = reinterpret_cast<uint32_t *>(p);
+    return SALE_B200_OK;
+}
+
+int upload_taus(sale_b200_ctx *ctx, const double *taus, int64_t n, cudaStream_t stream) {
+    if (n > ctx->taus_cap) {
+        if (ctx->d_taus) cudaFree(ctx->d_taus);
+        ctx->d_taus = nullptr;
+        SALE_CUDA(ctx, cudaMalloc(&ctx->d_taus, sizeof(double) * n));
+        ctx->taus_cap = n;
+    }
+    SALE_CUDA(ctx, cudaMemcpyAsync(ctx->d_taus, taus, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                   stream));
+    return SALE_B200_OK;
+}
+
+int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *q_codes,
+                const float *q_scales, const int8_t *k_codes, const float *k_scales,
+                const sale_b200_shape &s, const double *taus, uint32_t *mask, float *thresh,
+                const sale_b200_select_debug *dbg, cudaStream_t stream) {
+    int st;
+    if ((st = upload_taus(ctx, taus, s.q_heads, stream))) return st;
+    if ((st = ensure_units(ctx, s.tokens, stream))) return st;
+    const float isd = inv_sqrt_dim(s.head_dim);
+    SALE_CUDA(ctx, launch_base_mask(mask, s.batch, s.q_heads, s.tokens, stream));
+    SALE_CUDA(ctx, launch_sink_local_stats(q, k, s.batch, s.tokens, s.q_heads, s.kv_heads, isd,
+                                           ctx->d_taus, thresh, dbg ? dbg->running_max : nullptr,
+                                           dbg ? dbg->exp_sum : nullptr, dbg ? dbg->bound : nullptr,
+                                           stream));
+    if (ctx->n_units == 0) return SALE_B200_OK;
+    CUtensorMap tm_qc, tm_kc;
+    if ((st = make_map(ctx, &tm_qc, q_codes, false, s.batch, s.tokens, s.q_heads, 128, 128))) return st;
+    if ((st = make_map(ctx, &tm_kc, k_codes, false, s.batch, s.tokens, s.kv_heads, 128, 64))) return st;
+    SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_units, ctx->n_units, q_scales, k_scales,
+                                   thresh, mask, s.batch, s.tokens, static_cast<int>(s.q_heads),
+                                   static_cast<int>(s.kv_heads), isd,
+                                   dbg ? dbg->block_max : nullptr, stream));
+    return SALE_B200_OK;
+}
+
+int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                   const sale_b200_shape &s, const uint32_t *mask, void *out, int32_t *coverage,
+                   cudaStream_t stream) {
+    int st;
+    CUtensorMap tq, tk, tv;
+    if ((st = make_map(ctx, &tq, q, true, s.batch, s.tokens, s.q_heads, 64, 128))) return st;
+    if ((st = make_map(ctx, &tk, k, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
+    if ((st = make_map(ctx, &tv, v, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
+    const float scale_log2 = inv_sqrt_dim(s.head_dim) * 1.4426950408889634f;
+    SALE_CUDA(ctx, launch_sparse_attention(tq, tk, tv, mask, out, coverage, s.batch, s.tokens,
+                                           static_cast<int>(s.q_heads), static_cast<int>(s.kv_heads),
+                                           scale_log2, stream));
+    return SALE_B200_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+} // namespace
+
+extern "C" {
+
+int sale_b200_version(void) { return 1; }
+
+void sale_b200_default_config(sale_b200_selection_config *cfg) {
+    cfg->sink_tokens = 32;
+    cfg->local_tokens_min = 128;
+    cfg->segment_size = 4;
+    cfg->block_q = 64;
+    cfg->block_k = 32;
+}
+
+int sale_b200_ctx_create(int device, sale_b200_ctx **out) {
+    if (!out) return fail(nullptr, SALE_B200_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(nullptr, SALE_B200_CUDA_ERROR,
+                    std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= n) return fail(nullptr, SALE_B200_INVALID_ARGUMENT, "bad device");
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess)
+        return fail(nullptr, SALE_B200_CUDA_ERROR, cudaGetErrorString(e));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(nullptr, SALE_B200_UNSUPPORTED,
+                    "sale_b200 is built for sm_100a (B200); device is sm_" +
+                        std::to_string(prop.major) + std::to_string(prop.minor));
+    if ((e = cudaSetDevice(device)) != cudaSuccess)
+        return fail(nullptr, SALE_B200_CUDA_ERROR, cudaGetErrorString(e));
+    auto *ctx = new sale_b200_ctx();
+    ctx->device = device;
+    *out = ctx;
+    return SALE_B200_OK;
+}
+
+void sale_b200_ctx_destroy(sale_b200_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->d_taus) cudaFree(ctx->d_taus);
+    if (ctx->d_units) cudaFree(ctx->d_units);
+    if (ctx->io) cudaFree(ctx->io);
+    if (ctx->io_stream) cudaStreamDestroy(ctx->io_stream);
+    delete ctx;
+}
+
+const char *sale_b200_last_error(const sale_b200_ctx *ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+int sale_b200_quantize(sale_b200_ctx *ctx, const void *x, int64_t batch, int64_t tokens,
+                       int64_t heads, int64_t group_rows, int8_t *codes, float *scales,
+                       void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!x || !codes || !scales) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    if (batch < 1 || tokens < 1 || heads < 1)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "quantize: empty input");
+    if (group_rows < 1) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "QuantizedMatrix: group_rows must be >= 1");
+    if (group_rows != 1 && group_rows != kBlockK)
+        return fail(ctx, SALE_B200_UNSUPPORTED, "group_rows must be 1 (per token) or 32 (per key block)");
+    if (!aligned16(x) || !aligned16(codes))
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = group_rows == 1
+                        ? launch_quantize_qk(x, nullptr, codes, scales, nullptr, nullptr, batch,
+                                             tokens, heads, 1, s)
+                        : launch_quantize_qk(nullptr, x, nullptr, nullptr, codes, scales, batch,
+                                             tokens, 1, heads, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "quantize");
+    return SALE_B200_OK;
+}
+
+int sale_b200_quantize_qk(sale_b200_ctx *ctx, const void *q, const void *k,
+                          const sale_b200_shape *shape, int8_t *q_codes, float *q_scales,
+                          int8_t *k_codes, float *k_scales, void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int st;
+    if ((st = check_shape(ctx, shape))) return st;
+    if (!q || !k || !q_codes || !q_scales || !k_codes || !k_scales)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    SALE_CUDA(ctx, launch_quantize_qk(q, k, q_codes, q_scales, k_codes, k_scales, shape->batch,
+                                      shape->tokens, shape->q_heads, shape->kv_heads,
+                                      static_cast<cudaStream_t>(stream)));
+    return SALE_B200_OK;
+}
+
+int sale_b200_select(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *q_codes,
+                     const float *q_scales, const int8_t *k_codes, const float *k_scales,
+                     const sale_b200_shape *shape, const double *taus,
+                     const sale_b200_selection_config *cfg, uint32_t *mask_words,
+                     const sale_b200_select_debug *dbg, void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int st;
+    if ((st = check_shape(ctx, shape))) return st;
+    if ((st = check_config(ctx, cfg))) return st;
+    if ((st = check_taus(ctx, taus, shape->q_heads))) return st;
+    if (!q || !k || !q_codes || !q_scales || !k_codes || !k_scales || !mask_words)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    Workspace w;
+    if ((st = ensure_workspace(ctx, *shape, &w))) return st;
+    return select_impl(ctx, q, k, q_codes, q_scales, k_codes, k_scales, *shape, taus, mask_words,
+                       w.thresh, dbg, static_cast<cudaStream_t>(stream));
+}
+
+int sale_b200_sparse_attention(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                               const sale_b200_shape *shape, const uint32_t *mask_words,
+                               void *out, int32_t *coverage, void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int st;
+    if ((st = check_shape(ctx, shape))) return st;
+    if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    return attention_impl(ctx, q, k, v, *shape, mask_words, out, coverage,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int sale_b200_flop_count(sale_b200_ctx *ctx, const uint32_t *mask_words, int64_t batch,
+                         int64_t q_heads, int64_t tokens, int64_t *counts, void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!mask_words || !counts) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    if (batch < 1 || q_heads < 1 || tokens < 1)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "flop_accounting: empty grid");
+    SALE_CUDA(ctx, launch_flop_count(mask_words, batch, q_heads, tokens, counts,
+                                     static_cast<cudaStream_t>(stream)));
+    return SALE_B200_OK;
+}
+
+int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                      const sale_b200_shape *shape, const double *taus,
+                      const sale_b200_selection_config *cfg, void *out, uint32_t *mask_out,
+                      void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int st;
+    if ((st = check_shape(ctx, shape))) return st;
+    if ((st = check_config(ctx, cfg))) return st;
+    if ((st = check_taus(ctx, taus, shape->q_heads))) return st;
+    if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    Workspace w;
+    if ((st = ensure_workspace(ctx, *shape, &w))) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t *mask = mask_out ? mask_out : w.mask;
+    SALE_CUDA(ctx, launch_quantize_qk(q, k, w.q_codes, w.q_scales, w.k_codes, w.k_scales,
+                                      shape->batch, shape->tokens, shape->q_heads,
+                                      shape->kv_heads, s));
+    if ((st = select_impl(ctx, q, k, w.q_codes, w.q_scales, w.k_codes, w.k_scales, *shape, taus,
+                          mask, w.thresh, nullptr, s)))
+        return st;
+    return attention_impl(ctx, q, k, v, *shape, mask, out, nullptr, s);
+}
+
+int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t *k,
+                           const uint16_t *v, const sale_b200_shape *shape, const double *taus,
+                           const sale_b200_selection_config *cfg, uint16_t *out) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    int st;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if ((st = check_shape(ctx, shape))) return st;
+        if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+        const size_t qb = align256(2 * shape->batch * shape->tokens * shape->q_heads * kHeadDim);
+        const size_t kb = align256(2 * shape->batch * shape->tokens * shape->kv_heads * kHeadDim);
+        const size_t need = 2 * qb + 2 * kb;
+        if (need > ctx->io_bytes) {
+            if (ctx->io) cudaFree(ctx->io);
+            ctx->io = nullptr;
+            ctx->io_bytes = 0;
+            SALE_CUDA(ctx, cudaMalloc(&ctx->io, need));
+            ctx->io_bytes = need;
+        }
+        if (!ctx->io_stream)
+            SALE_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->io_stream, cudaStreamNonBlocking));
+    }
+    const size_t qbytes = 2 * shape->batch * shape->tokens * shape->q_heads * kHeadDim;
+    const size_t kbytes = 2 * shape->batch * shape->tokens * shape->kv_heads * kHeadDim;
+    uint8_t *dq = ctx->io, *dk = dq + align256(qbytes), *dv = dk + align256(kbytes),
+            *dout = dv + align256(kbytes);
+    cudaStream_t s = ctx->io_stream;
+    SALE_CUDA(ctx, cudaMemcpyAsync(dq, q, qbytes, cudaMemcpyHostToDevice, s));
+    SALE_CUDA(ctx, cudaMemcpyAsync(dk, k, kbytes, cudaMemcpyHostToDevice, s));
+    SALE_CUDA(ctx, cudaMemcpyAsync(dv, v, kbytes, cudaMemcpyHostToDevice, s));
+    if ((st = sale_b200_prefill(ctx, dq, dk, dv, shape, taus, cfg, dout, nullptr, s))) return st;
+    SALE_CUDA(ctx, cudaMemcpyAsync(out, dout, qbytes, cudaMemcpyDeviceToHost, s));
+    SALE_CUDA(ctx, cudaStreamSynchronize(s));
+    return SALE_B200_OK;
+}
+
+} // extern "C"

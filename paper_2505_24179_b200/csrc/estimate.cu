@@ -1,0 +1,261 @@
+// estimate.cu — K2b: the low-bit Q.K^T estimator of the Selection-Pass on the
+// 5th-gen tensor cores (tcgen05.mma kind::i8, int32 accumulators in TMEM).
+//
+// Replaces the CPU hot loop approx_weight_block (quant.hpp:136-166) +
+// max_then_dequantize (quant.hpp:170-179) + the relative-score decision and
+// segment OR of selection_pass (selection.hpp:253-271).
+//
+// Work unit (one CTA): one (batch, KV head, <=4 query heads of that GQA group)
+// x one 128-row query tile x a chunk of up to kSegPerUnit middle segments.
+//   * The 128-row tile pairs query blocks (2m+1, 2m+2): both have the same
+//     full-segment count F = m-1, so one key range
+//     serves both. A = 4 heads x [128 rows x 128 int8 codes] (64 KB, loaded once).
+//   * Keys stream through an 8-deep TMA ring of 64-key stages (8 KB each); the
+//     same K-code stage feeds all 4 heads (M = 512 effective rows per byte of K).
+//   * Per stage: 4 heads x 4 MMAs (K=32) of M=128,N=64 into one of two 256-column
+//     TMEM buffers, so the epilogue drains buffer b while the MMA fills b^1.
+//   * Epilogue (8 warps, thread = row): tcgen05.ld .pack::16b (products fit in
+//     int16: |p| <= 128*49), 16-bit SIMD max per 32-key block, then
+//     est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max and est >= fb_row,
+//     exactly the reference's float arithmetic. Rows OR per segment with a warp
+//     vote; segments are OR-ed into the packed mask with atomicOr.
+#include "common.cuh"
+#include "internal.h"
+
+namespace sale_b200 {
+
+constexpr int kSegPerUnit = 16;           // segments per work unit (2048 keys)
+constexpr int kEstHeads = 4;               // query heads per CTA
+constexpr int kEstStages = 8;              // TMA ring depth
+constexpr int kStageKeys = 64;             // keys per stage (2 key blocks)
+constexpr int kATileBytes = 128 * kHeadDim;        // 16 KB per head
+constexpr int kBStageBytes = kStageKeys * kHeadDim; // 8 KB
+constexpr int kEstThreads = 384;           // warps 0-3 control, 4-11 epilogue
+
+struct EstSmem {
+    alignas(1024) uint8_t a[kEstHeads][kATileBytes];
+    alignas(1024) uint8_t bst[kEstStages][kBStageBytes];
+    uint64_t full[kEstStages];
+    uint64_t empty[kEstStages];
+    uint64_t a_full;
+    uint64_t tmem_full[2];
+    uint64_t tmem_empty[2];
+    uint32_t tmem_base;
+    uint32_t seg_bits[kEstHeads][2];
+};
+
+static_assert(kSegPerUnit == kSegPerUnitHost, "unit size mismatch");
+
+namespace {
+
+__global__ void __launch_bounds__(kEstThreads, 1)
+estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_kc,
+                const EstUnit *__restrict__ units, const float *__restrict__ q_scales,
+                const float *__restrict__ k_scales, const float *__restrict__ thresh,
+                uint32_t *__restrict__ mask, int64_t tokens, int hq, int hkv, int nsub,
+                float inv_sqrt_d, int32_t *__restrict__ dbg_max) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // dynamic smem base is only 16-B aligned by contract: round up to 1 KB
+    EstSmem &sm = *reinterpret_cast<EstSmem *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    const EstUnit u = units[blockIdx.x];
+    const int y = blockIdx.y;
+    const int sub = y % nsub;
+    const int g = (y / nsub) % hkv;
+    const int b = y / (nsub * hkv);
+    const int group = hq / hkv;
+    const int h0 = g * group + sub * kEstHeads;
+    const int nh = min(kEstHeads, group - sub * kEstHeads);
+    const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
+    const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
+    const int64_t words = (nk + 31) / 32;
+    const int nstages = 2 * u.nseg;
+    const int row0 = 128 * u.m + 64;
+    const int key_base = kBlockK + kSegment * kBlockK * kSegPerUnit * u.c; // first key of the unit
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kEstStages; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+        }
+        mbar_init(&sm.a_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.tmem_full[s], 1);
+            mbar_init(&sm.tmem_empty[s], 8);
+        }
+        for (int hh = 0; hh < kEstHeads; ++hh) sm.seg_bits[hh][0] = sm.seg_bits[hh][1] = 0;
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------- TMA producer
+        if (elect_one()) {
+            tma_prefetch(&tm_qc);
+            tma_prefetch(&tm_kc);
+            mbar_expect_tx(&sm.a_full, static_cast<uint32_t>(nh * kATileBytes));
+            for (int hh = 0; hh < nh; ++hh)
+                tma_load_4d(sm.a[hh], &tm_qc, &sm.a_full, 0, h0 + hh, row0, b);
+            for (int k = 0; k < nstages; ++k) {
+                const int st = k % kEstStages;
+                mbar_wait(&sm.empty[st], ((k / kEstStages) & 1) ^ 1);
+                mbar_expect_tx(&sm.full[st], kBStageBytes);
+                tma_load_4d(sm.bst[st], &tm_kc, &sm.full[st], 0, g, key_base + kStageKeys * k, b);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (elect_one()) {
+            constexpr uint32_t idesc = idesc_i8(128, kStageKeys);
+            uint64_t adesc[kEstHeads];
+            for (int hh = 0; hh < kEstHeads; ++hh) adesc[hh] = umma_desc_sw128(smem_u32(sm.a[hh]), 16, 1024);
+            mbar_wait(&sm.a_full, 0);
+            tc_fence_after();
+            for (int k = 0; k < nstages; ++k) {
+                const int st = k % kEstStages;
+                const int bb = k & 1;
+                mbar_wait(&sm.full[st], (k / kEstStages) & 1);
+                mbar_wait(&sm.tmem_empty[bb], ((k >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.bst[st]), 16, 1024);
+                for (int hh = 0; hh < nh; ++hh) {
+                    const uint32_t d = tmem + bb * 256 + hh * kStageKeys;
+#pragma unroll
+                    for (int kk = 0; kk < kHeadDim / 32; ++kk)
+                        mma_i8_ss(d, adesc[hh] + 2 * kk, bdesc + 2 * kk, idesc, kk > 0);
+                }
+                tc_commit(&sm.empty[st]);
+                tc_commit(&sm.tmem_full[bb]);
+            }
+        }
+    } else if (warp >= 4) {
+        // -------------------------------------------------------------- epilogue
+        const int ew = warp - 4;
+        const int quad = warp & 3;            // TMEM lane quadrant this warp may access
+        const int r = quad * 32 + lane;       // row within the 128-row tile
+        const int64_t tok = row0 + r;
+        const bool row_ok = tok < tokens;
+        const int hA = ew >> 2, hB = hA + 2;  // this warp's two heads
+        float qs[2], fb[2];
+        bool flag[2] = {false, false};
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            const int hh = x == 0 ? hA : hB;
+            qs[x] = 0.0f;
+            fb[x] = INFINITY;
+            if (row_ok && hh < nh) {
+                const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
+                qs[x] = q_scales[o];
+                fb[x] = thresh[o];
+            }
+        }
+        const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        for (int k = 0; k < nstages; ++k) {
+            const int bb = k & 1;
+            const int64_t jb0 = (key_base + kStageKeys * k) / kBlockK;
+            const float* ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
+            const float ks0 = ks_row[jb0], ks1 = ks_row[jb0 + 1];
+            mbar_wait(&sm.tmem_full[bb], (k >> 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const int hh = x == 0 ? hA : hB;
+                if (hh >= nh) continue; // warp-uniform
+#pragma unroll
+                for (int jb = 0; jb < 2; ++jb) {
+                    uint32_t v[16];
+                    tmem_ld32_pack16(lane_addr + bb * 256 + hh * kStageKeys + jb * 32, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int s = 8; s > 0; s >>= 1)
+#pragma unroll
+                        for (int e = 0; e < s; ++e) v[e] = __vmaxs2(v[e], v[e + s]);
+                    const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
+                    const int hi = static_cast<int16_t>(v[0] >> 16);
+                    const int mx = lo > hi ? lo : hi;
+                    const float rs = __fmul_rn(__fmul_rn(qs[x], jb ? ks1 : ks0), inv_sqrt_d);
+                    const float est = __fmul_rn(rs, static_cast<float>(mx));
+                    flag[x] |= est >= fb[x];
+                    if (dbg_max != nullptr && row_ok)
+                        dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                                jb0 + jb] = mx;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.tmem_empty[bb]);
+            if (k & 1) {
+                const int seg = k >> 1;
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    const int hh = x == 0 ? hA : hB;
+                    if (hh >= nh) continue;
+                    const bool any = __any_sync(0xffffffffu, flag[x]);
+                    if (lane == 0 && any) atomicOr(&sm.seg_bits[hh][quad >> 1], 1u << seg);
+                    flag[x] = false;
+                }
+            }
+        }
+        named_bar_sync(1, 256);
+        if (ew == 0 && lane < 2 * kEstHeads) {
+            const int hh = lane >> 1, half = lane & 1;
+            const int64_t qi = 2 * static_cast<int64_t>(u.m) + 1 + half;
+            uint32_t bits = sm.seg_bits[hh][half];
+            if (hh < nh && qi < nq && bits) {
+                uint32_t *row = mask + ((static_cast<int64_t>(b) * hq + h0 + hh) * nq + qi) * words;
+                while (bits) {
+                    const int s = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const int64_t sg = static_cast<int64_t>(kSegPerUnit) * u.c + s;
+                    const int64_t j0 = 1 + kSegment * sg; // blocks j0 .. j0+3
+                    const uint32_t w0 = static_cast<uint32_t>(j0 >> 5), sh = j0 & 31;
+                    atomicOr(row + w0, 0xFu << sh);
+                    if (sh > 28) atomicOr(row + w0 + 1, 0xFu >> (32 - sh));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+} // namespace
+
+size_t estimate_smem_bytes() { return sizeof(EstSmem) + 1024; }
+
+cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
+                            int64_t n_units, const float *q_scales, const float *k_scales,
+                            const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
+                            int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
+                            cudaStream_t stream) {
+    if (n_units == 0) return cudaSuccess;
+    static bool configured = false;
+    const size_t smem = estimate_smem_bytes();
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(estimate_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int group = hq / hkv;
+    const int nsub = (group + kEstHeads - 1) / kEstHeads;
+    dim3 grid(static_cast<unsigned>(n_units), static_cast<unsigned>(batch * hkv * nsub));
+    estimate_kernel<<<grid, kEstThreads, smem, stream>>>(tm_qc, tm_kc, units, q_scales, k_scales,
+                                                         thresh, mask, tokens, hq, hkv, nsub,
+                                                         inv_sqrt_d, dbg_max);
+    return cudaGetLastError();
+}
+
+} // namespace sale_b200

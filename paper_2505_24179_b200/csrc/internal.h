@@ -1,0 +1,45 @@
+// internal.h — launcher declarations shared between the kernels and the C ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace sale_b200 {
+
+struct EstUnit {
+    int m;    // 128-row query tile: rows [128m+64, 128m+192) = query blocks 2m+1, 2m+2
+    int c;    // chunk of kSegPerUnit middle segments
+    int nseg; // segments in this unit
+};
+constexpr int kSegPerUnitHost = 16;
+
+cudaError_t launch_quantize_qk(const void *q, const void *k, int8_t *q_codes, float *q_scales,
+                               int8_t *k_codes, float *k_scales, int64_t batch, int64_t tokens,
+                               int64_t hq, int64_t hkv, cudaStream_t stream);
+
+cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch, int64_t tokens,
+                                    int64_t hq, int64_t hkv, float inv_sqrt_d, const double *taus,
+                                    float *thresh, double *dbg_m, double *dbg_l, double *dbg_bound,
+                                    cudaStream_t stream);
+
+cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
+                             cudaStream_t stream);
+
+size_t estimate_smem_bytes();
+cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
+                            int64_t n_units, const float *q_scales, const float *k_scales,
+                            const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
+                            int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
+                            cudaStream_t stream);
+
+size_t attention_smem_bytes();
+cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &tm_k,
+                                    const CUtensorMap &tm_v, const uint32_t *mask, void *out,
+                                    int32_t *coverage, int64_t batch, int64_t tokens, int hq,
+                                    int hkv, float scale_log2, cudaStream_t stream);
+
+cudaError_t launch_flop_count(const uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
+                              int64_t *counts, cudaStream_t stream);
+
+} // namespace sale_b200

@@ -1,0 +1,358 @@
+"""Python host mirror of the reference's hot-path API over the C ABI.
+
+Same names and argument meaning as the reference's `namespace sale`
+(/root/reference/proj/include/sale), lifted from one head of fp32 to the
+B200 layout: bf16 torch tensors [B, N, H, 128] on the GPU (rows zero-padded
+past head_dim). Every call goes through lib/libsale_b200.so (include/sale_b200.h);
+there is no CPU fallback — a missing library or a non-sm_100 device raises.
+
+Error classes follow the reference: ValueError for std::invalid_argument,
+ArithmeticError for std::domain_error, IndexError for std::out_of_range,
+RuntimeError for CUDA failures and NotImplementedError for configurations the
+B200 path does not implement.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsale_b200.so")
+
+BLOCK_Q, BLOCK_K, SEGMENT, HEAD_PITCH = 64, 32, 4, 128
+
+i64 = C.c_int64
+vp = C.c_void_p
+
+
+class Shape(C.Structure):
+    _fields_ = [("batch", i64), ("tokens", i64), ("q_heads", i64), ("kv_heads", i64),
+                ("head_dim", i64)]
+
+
+class SelectionConfig(C.Structure):
+    """sale::SelectionConfig (selection.hpp:18-24) minus tau (per head)."""
+
+    _fields_ = [("sink_tokens", i64), ("local_tokens_min", i64), ("segment_size", i64),
+                ("block_q", i64), ("block_k", i64)]
+
+
+def default_config() -> SelectionConfig:
+    return SelectionConfig(32, 128, 4, 64, 32)
+
+
+class SelectDebug(C.Structure):
+    _fields_ = [("running_max", vp), ("exp_sum", vp), ("bound", vp), ("block_max", vp)]
+
+
+_ERRORS = {1: ValueError, 2: ArithmeticError, 3: IndexError, 4: RuntimeError,
+           5: NotImplementedError}
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Loads lib/libsale_b200.so (built by `make -C paper_2505_24179_b200`)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: build it with __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    sig = {
+        "sale_b200_ctx_create": (C.c_int, [C.c_int, P(vp)]),
+        "sale_b200_ctx_destroy": (None, [vp]),
+        "sale_b200_last_error": (C.c_char_p, [vp]),
+        "sale_b200_version": (C.c_int, []),
+        "sale_b200_default_config": (None, [P(SelectionConfig)]),
+        "sale_b200_quantize": (C.c_int, [vp, vp, i64, i64, i64, i64, vp, vp, vp]),
+        "sale_b200_quantize_qk": (C.c_int, [vp, vp, vp, P(Shape), vp, vp, vp, vp, vp]),
+        "sale_b200_select": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, P(Shape), P(C.c_double),
+                                       P(SelectionConfig), vp, P(SelectDebug), vp]),
+        "sale_b200_sparse_attention": (C.c_int, [vp, vp, vp, vp, P(Shape), vp, vp, vp, vp]),
+        "sale_b200_flop_count": (C.c_int, [vp, vp, i64, i64, i64, vp, vp]),
+        "sale_b200_prefill": (C.c_int, [vp, vp, vp, vp, P(Shape), P(C.c_double),
+                                        P(SelectionConfig), vp, vp, vp]),
+        "sale_b200_prefill_host": (C.c_int, [vp, vp, vp, vp, P(Shape), P(C.c_double),
+                                             P(SelectionConfig), vp]),
+        "sale_b200_workload_head_f32": (C.c_int, [C.c_int, C.c_uint64, i64, i64, i64, vp, vp, vp]),
+        "sale_b200_workload_gqa_bf16": (C.c_int, [C.c_int, C.c_uint64, P(Shape), vp, vp, vp,
+                                                  C.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Context:
+    """sale_b200_ctx on one device (one stream at a time)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        self.handle = vp()
+        self.device = device
+        self._check(self.lib.sale_b200_ctx_create(device, C.byref(self.handle)), create=True)
+
+    def _check(self, status, create=False):
+        if status:
+            msg = self.lib.sale_b200_last_error(None if create else self.handle)
+            raise _ERRORS.get(status, RuntimeError)((msg or b"").decode())
+
+    def close(self):
+        if self.handle:
+            self.lib.sale_b200_ctx_destroy(self.handle)
+            self.handle = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_ctx: Context | None = None
+
+
+def context() -> Context:
+    global _ctx
+    if _ctx is None:
+        import torch
+        _ctx = Context(torch.cuda.current_device())
+    return _ctx
+
+
+# ------------------------------------------------------------------ geometry
+
+def grid(tokens: int):
+    nq = -(-tokens // BLOCK_Q)
+    nk = -(-tokens // BLOCK_K)
+    return nq, nk, -(-nk // 32)
+
+
+def unpack_mask(words, tokens: int) -> np.ndarray:
+    """Packed mask words (any leading dims, last = words) -> uint8 [..., Nq, Nk]
+    (the sale::BlockMask cell layout, selection.hpp:84)."""
+    w = np.ascontiguousarray(np.asarray(words).astype(np.uint32))
+    nq, nk, nw = grid(tokens)
+    bits = np.unpackbits(w.view(np.uint8).reshape(*w.shape[:-1], nw * 4), axis=-1,
+                         bitorder="little")
+    return bits[..., :nk].astype(np.uint8)
+
+
+def pack_mask(cells: np.ndarray, tokens: int) -> np.ndarray:
+    """uint8 [..., Nq, Nk] -> uint32 words [..., Nq, W] (inverse of unpack_mask)."""
+    nq, nk, nw = grid(tokens)
+    cells = np.asarray(cells, np.uint8)
+    pad = np.zeros((*cells.shape[:-1], nw * 32), np.uint8)
+    pad[..., :nk] = cells != 0
+    return np.packbits(pad, axis=-1, bitorder="little").view(np.uint32)
+
+
+# ---------------------------------------------------------- stage wrappers
+
+def _shape_of(q, k, head_dim):
+    B, N, Hq, P = q.shape
+    if P != HEAD_PITCH:
+        raise ValueError("rows must be padded to 128 elements")
+    return Shape(B, N, Hq, k.shape[2], head_dim)
+
+
+def quantize_qk(q, k, head_dim=128):
+    """quantize_per_token(Q) + quantize_per_key_block(K) (quant.hpp:95/107), fused.
+    Returns (q_codes int8 [B,N,Hq,128], q_scales f32 [B,Hq,N],
+             k_codes int8 [B,N,Hkv,128], k_scales f32 [B,Hkv,Nk])."""
+    import torch
+    ctx = context()
+    s = _shape_of(q, k, head_dim)
+    _, nk, _ = grid(s.tokens)
+    qc = torch.empty(q.shape, dtype=torch.int8, device=q.device)
+    kc = torch.empty(k.shape, dtype=torch.int8, device=k.device)
+    qs = torch.empty((s.batch, s.q_heads, s.tokens), dtype=torch.float32, device=q.device)
+    ks = torch.empty((s.batch, s.kv_heads, nk), dtype=torch.float32, device=q.device)
+    ctx._check(ctx.lib.sale_b200_quantize_qk(ctx.handle, _ptr(q), _ptr(k), C.byref(s), _ptr(qc),
+                                             _ptr(qs), _ptr(kc), _ptr(ks), _stream()))
+    return qc, qs, kc, ks
+
+
+def quantize_per_token(x):
+    """quant.hpp:95 for every (batch, head) of x [B,N,H,128]."""
+    import torch
+    ctx = context()
+    B, N, H, _ = x.shape
+    codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
+    scales = torch.empty((B, H, N), dtype=torch.float32, device=x.device)
+    ctx._check(ctx.lib.sale_b200_quantize(ctx.handle, _ptr(x), B, N, H, 1, _ptr(codes),
+                                          _ptr(scales), _stream()))
+    return codes, scales
+
+
+def quantize_per_key_block(x):
+    """quant.hpp:107 (block_k = 32) for every (batch, head) of x [B,N,H,128]."""
+    import torch
+    ctx = context()
+    B, N, H, _ = x.shape
+    codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
+    scales = torch.empty((B, H, grid(N)[1]), dtype=torch.float32, device=x.device)
+    ctx._check(ctx.lib.sale_b200_quantize(ctx.handle, _ptr(x), B, N, H, BLOCK_K, _ptr(codes),
+                                          _ptr(scales), _stream()))
+    return codes, scales
+
+
+@dataclass
+class SelectDebugOut:
+    running_max: object
+    exp_sum: object
+    bound: object
+    block_max: object
+
+
+def selection_pass(q, k, q_codes, q_scales, k_codes, k_scales, taus, head_dim=128,
+                   config: SelectionConfig | None = None, debug=False):
+    """selection.hpp:211 for every (batch, q head). taus: one per q head.
+    Returns packed mask words int32 [B,Hq,Nq,W] (and SelectDebugOut)."""
+    import torch
+    ctx = context()
+    s = _shape_of(q, k, head_dim)
+    nq, nk, nw = grid(s.tokens)
+    taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (s.q_heads,)))
+    mask = torch.empty((s.batch, s.q_heads, nq, nw), dtype=torch.int32, device=q.device)
+    dbg_struct = None
+    dbg = None
+    if debug:
+        f = dict(dtype=torch.float64, device=q.device)
+        dbg = SelectDebugOut(torch.full((s.batch, s.q_heads, s.tokens), float("nan"), **f),
+                             torch.full((s.batch, s.q_heads, s.tokens), float("nan"), **f),
+                             torch.full((s.batch, s.q_heads, s.tokens), float("nan"), **f),
+                             torch.full((s.batch, s.q_heads, s.tokens, nk), -2 ** 31,
+                                        dtype=torch.int32, device=q.device))
+        dbg_struct = SelectDebug(dbg.running_max.data_ptr(), dbg.exp_sum.data_ptr(),
+                                 dbg.bound.data_ptr(), dbg.block_max.data_ptr())
+    cfg = config if config is not None else default_config()
+    ctx._check(ctx.lib.sale_b200_select(
+        ctx.handle, _ptr(q), _ptr(k), _ptr(q_codes), _ptr(q_scales), _ptr(k_codes),
+        _ptr(k_scales), C.byref(s), taus.ctypes.data_as(C.POINTER(C.c_double)), C.byref(cfg),
+        _ptr(mask), C.byref(dbg_struct) if dbg_struct is not None else None, _stream()))
+    return (mask, dbg) if debug else mask
+
+
+def block_sparse_attention(q, k, v, mask=None, head_dim=128, coverage=False):
+    """sparse_attention.hpp:37 (mask = packed words) or, with mask=None,
+    full_attention (attention.hpp:18). Returns out bf16 [B,N,Hq,128]
+    (and coverage int32 [B,Hq,N])."""
+    import torch
+    ctx = context()
+    s = _shape_of(q, k, head_dim)
+    out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
+    cov = (torch.empty((s.batch, s.q_heads, s.tokens), dtype=torch.int32, device=q.device)
+           if coverage else None)
+    ctx._check(ctx.lib.sale_b200_sparse_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v),
+                                                  C.byref(s), _ptr(mask), _ptr(out), _ptr(cov),
+                                                  _stream()))
+    return (out, cov) if coverage else out
+
+
+def full_attention(q, k, v, head_dim=128):
+    return block_sparse_attention(q, k, v, None, head_dim)
+
+
+def flop_accounting(mask, tokens):
+    """sparse_attention.hpp:101 per (batch, head): int64 [B,Hq,3] =
+    (computed, skipped, total) causal blocks."""
+    import torch
+    ctx = context()
+    B, H = mask.shape[0], mask.shape[1]
+    counts = torch.empty((B, H, 3), dtype=torch.int64, device=mask.device)
+    ctx._check(ctx.lib.sale_b200_flop_count(ctx.handle, _ptr(mask), B, H, tokens, _ptr(counts),
+                                            _stream()))
+    return counts
+
+
+def prefill(q, k, v, taus, head_dim=128, mask_out=None, config=None):
+    """run_pipeline's stage composition (runner.hpp:63-80) on device tensors:
+    quantize -> selection -> block-sparse attention. Returns out bf16."""
+    import torch
+    ctx = context()
+    s = _shape_of(q, k, head_dim)
+    taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (s.q_heads,)))
+    out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
+    cfg = config if config is not None else default_config()
+    ctx._check(ctx.lib.sale_b200_prefill(ctx.handle, _ptr(q), _ptr(k), _ptr(v), C.byref(s),
+                                         taus.ctypes.data_as(C.POINTER(C.c_double)), C.byref(cfg),
+                                         _ptr(out), _ptr(mask_out), _stream()))
+    return out
+
+
+def prefill_host(q, k, v, taus, out, head_dim=128, config=None):
+    """End to end from host buffers (numpy uint16 / pinned torch bf16 on CPU):
+    H2D + the three stages + D2H of out, synchronous."""
+    ctx = context()
+    ptr = (lambda a: C.c_void_p(a.ctypes.data)) if isinstance(q, np.ndarray) else _ptr
+    B, N, Hq, _ = q.shape
+    s = Shape(B, N, Hq, k.shape[2], head_dim)
+    taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (Hq,)))
+    cfg = config if config is not None else default_config()
+    ctx._check(ctx.lib.sale_b200_prefill_host(ctx.handle, ptr(q), ptr(k), ptr(v), C.byref(s),
+                                              taus.ctypes.data_as(C.POINTER(C.c_double)),
+                                              C.byref(cfg), ptr(out)))
+    return out
+
+
+# ------------------------------------------------------------- workloads
+
+def workload_head_f32(kind: str, seed: int, tokens: int, dim: int, head: int = 0):
+    """workloads.hpp gaussian_head / sink_local_head: (q, k, v) fp32 [n, d]."""
+    lib = load_library()
+    q, k, v = (np.empty((tokens, dim), np.float32) for _ in range(3))
+    st = lib.sale_b200_workload_head_f32({"gaussian": 0, "sink_local": 1}[kind], seed, tokens,
+                                         dim, head, q.ctypes.data, k.ctypes.data, v.ctypes.data)
+    if st:
+        raise ValueError(f"workload_head_f32: status {st}")
+    return q, k, v
+
+
+def workload_gqa(kind: str, seed: int, batch: int, tokens: int, q_heads: int, kv_heads: int,
+                 head_dim: int = 128, threads: int = 0, out=None):
+    """GQA extension of the reference generator as bf16 bit
+    patterns: uint16 q [B,N,Hq,128], k, v [B,N,Hkv,128] (numpy, host)."""
+    lib = load_library()
+    if out is None:
+        q = np.empty((batch, tokens, q_heads, HEAD_PITCH), np.uint16)
+        k = np.empty((batch, tokens, kv_heads, HEAD_PITCH), np.uint16)
+        v = np.empty((batch, tokens, kv_heads, HEAD_PITCH), np.uint16)
+    else:
+        q, k, v = out
+    s = Shape(batch, tokens, q_heads, kv_heads, head_dim)
+    st = lib.sale_b200_workload_gqa_bf16({"gaussian": 0, "sink_local": 1}[kind], seed,
+                                         C.byref(s), q.ctypes.data, k.ctypes.data,
+                                         v.ctypes.data, threads)
+    if st:
+        raise ValueError(f"workload_gqa: status {st}")
+    return q, k, v
+
+
+def bf16_bits_to_f32(a: np.ndarray) -> np.ndarray:
+    return (np.asarray(a, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def f32_to_bf16_bits(a: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16 bit patterns (finite inputs)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return u.astype(np.uint16)

@@ -1,0 +1,239 @@
+"""GPU parity: every stage of the B200 path through the C ABI against the
+oracle on identical bf16 inputs.
+
+Bars (BASELINE.json north_star): codes, scales, integer block maxima and
+masks bit-exact; running max bit-exact; exp_sum within 2 ulp (CUDA vs glibc
+double exp); attention output within 2e-2 max-abs and 1e-3 mean-abs of the
+oracle's block_sparse_attention on the same mask (bf16 MMA, fp32 accumulate).
+"""
+import numpy as np
+import pytest
+
+from helpers import Inputs, O, max_abs, mean_abs, oracle_quant, oracle_select
+from paper_2505_24179_b200 import sale
+
+pytestmark = pytest.mark.gpu
+
+ATOL_MAX = 2e-2
+ATOL_MEAN = 1e-3
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available(), "GPU tests need a B200"
+    return t
+
+
+def _to_np(t):
+    return t.detach().cpu().numpy()
+
+
+# ------------------------------------------------------------------ stage 1
+
+@pytest.mark.parametrize("kind,N,Hq,Hkv,d", [("sink_local", 1000, 4, 2, 128),
+                                              ("gaussian", 517, 8, 8, 128),
+                                              ("sink_local", 300, 4, 1, 64),
+                                              ("gaussian", 33, 2, 1, 16)])
+def test_quantize_bit_exact(torch, kind, N, Hq, Hkv, d):
+    inp = Inputs(kind, 11, 2, N, Hq, Hkv, d)
+    q, k, _ = inp.torch()
+    qc, qs, kc, ks = (_to_np(x) for x in sale.quantize_qk(q, k, d))
+    qq, kq = oracle_quant(inp)
+    for b in range(inp.B):
+        for h in range(Hq):
+            np.testing.assert_array_equal(qc[b, :, h, :d], qq[(b, h)][0])
+            assert (qc[b, :, h, d:] == 0).all()
+            np.testing.assert_array_equal(qs[b, h], qq[(b, h)][1])
+        for g in range(Hkv):
+            np.testing.assert_array_equal(kc[b, :, g, :d], kq[(b, g)][0])
+            np.testing.assert_array_equal(ks[b, g], kq[(b, g)][1])
+    # the standalone entry points agree with the fused launch
+    qc2, qs2 = sale.quantize_per_token(q)
+    kc2, ks2 = sale.quantize_per_key_block(k)
+    np.testing.assert_array_equal(_to_np(qc2), qc)
+    np.testing.assert_array_equal(_to_np(ks2), ks)
+
+
+def test_quantize_hand_rows(torch):
+    # test_quant.cpp:16-33: [7,-7,3.5,0] -> codes [7,-7,4,0] (half away from
+    # zero), scale 1; an all-zero row gets scale 1 and zero codes.
+    x = np.zeros((1, 2, 1, 128), np.float32)
+    x[0, 0, 0, :4] = [7.0, -7.0, 3.5, 0.0]
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    codes, scales = sale.quantize_per_token(xt)
+    codes, scales = _to_np(codes), _to_np(scales)
+    assert list(codes[0, 0, 0, :4]) == [7, -7, 4, 0]
+    assert scales[0, 0, 0] == 1.0 and scales[0, 0, 1] == 1.0
+    assert (codes[0, 1] == 0).all()
+
+
+# ------------------------------------------------------------------ stage 2
+
+def _check_selection(inp, taus, dbg_check=True):
+    import torch
+    q, k, _ = inp.torch()
+    qc, qs, kc, ks = sale.quantize_qk(q, k, inp.d)
+    mask, dbg = sale.selection_pass(q, k, qc, qs, kc, ks, taus, inp.d, debug=True)
+    torch.cuda.synchronize()
+    cells = sale.unpack_mask(_to_np(mask), inp.N)
+    ref = oracle_select(inp, taus, debug=True)
+    m, l, bound, bmax = (_to_np(x) for x in (dbg.running_max, dbg.exp_sum, dbg.bound,
+                                             dbg.block_max))
+    for (b, h), (rmask, rdbg) in ref.items():
+        np.testing.assert_array_equal(cells[b, h], rmask, err_msg=f"mask b={b} h={h}")
+        if not dbg_check:
+            continue
+        est = ~np.isnan(rdbg["m"])
+        np.testing.assert_array_equal(m[b, h][est], rdbg["m"][est])
+        # exp_sum: CUDA double exp (<=1 ulp) vs glibc -> allow 2 ulp
+        np.testing.assert_allclose(l[b, h][est], rdbg["l"][est], rtol=4.5e-16, atol=0)
+        np.testing.assert_allclose(bound[b, h][est], rdbg["bound"][est], rtol=1e-15, atol=1e-15)
+        ok = rdbg["block_max"] != np.iinfo(np.int32).min
+        np.testing.assert_array_equal(bmax[b, h][ok], rdbg["block_max"][ok])
+    return cells, ref
+
+
+@pytest.mark.parametrize("N", [2048, 1000, 200])
+def test_selection_bit_exact_small(torch, N):
+    inp = Inputs("sink_local", 7, 1, N, 8, 2)
+    _check_selection(inp, [0.004, 0.05, 0.004, 1e-9, 0.5, 0.004, 0.016, 0.1])
+
+
+def test_selection_llama_4k(torch):
+    """configs[0]: Llama-3.1-8B shape (32 Q / 8 KV heads), seq 4K, tau 0.004."""
+    inp = Inputs("sink_local", 7, 1, 4096, 32, 8)
+    _check_selection(inp, 0.004)
+
+
+def test_selection_gaussian_batch(torch):
+    inp = Inputs("gaussian", 3, 2, 1536, 4, 1)
+    _check_selection(inp, 0.004)
+
+
+# ------------------------------------------------------------------ stage 3
+
+def _oracle_attention(inp, cells, heads):
+    def one(i):
+        b, h = heads[i]
+        g = h // inp.G
+        m = cells[b, h] if cells is not None else None
+        if m is None:
+            return O.full_attention(inp.qh(b, h), inp.kh(b, g), inp.vh(b, g)), None, 0
+        return O.block_sparse_attention(inp.qh(b, h), inp.kh(b, g), inp.vh(b, g), m)
+    return dict(zip(heads, O.map_heads(one, len(heads))))
+
+
+@pytest.mark.parametrize("kind,N,Hq,Hkv", [("gaussian", 1024, 4, 1), ("sink_local", 777, 2, 2),
+                                           ("sink_local", 64, 2, 1), ("gaussian", 129, 2, 1)])
+def test_dense_attention(torch, kind, N, Hq, Hkv):
+    inp = Inputs(kind, 5, 1, N, Hq, Hkv)
+    q, k, v = inp.torch()
+    out, cov = sale.block_sparse_attention(q, k, v, None, inp.d, coverage=True)
+    out = _to_np(out.float())
+    cov = _to_np(cov)
+    ref = _oracle_attention(inp, None, inp.heads())
+    for (b, h), (o, _, _) in ref.items():
+        got = out[b, :, h, :inp.d]
+        assert max_abs(got, o) < ATOL_MAX, (b, h, max_abs(got, o))
+        assert mean_abs(got, o) < ATOL_MEAN, (b, h, mean_abs(got, o))
+        np.testing.assert_array_equal(cov[b, h], np.arange(1, N + 1))
+
+
+def test_sparse_attention_selected_mask(torch):
+    inp = Inputs("sink_local", 7, 1, 2048, 8, 2)
+    q, k, v = inp.torch()
+    qc, qs, kc, ks = sale.quantize_qk(q, k)
+    mask = sale.selection_pass(q, k, qc, qs, kc, ks, 0.004)
+    out, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True)
+    cells = sale.unpack_mask(_to_np(mask), inp.N)
+    ref = _oracle_attention(inp, cells, inp.heads())
+    out, cov = _to_np(out.float()), _to_np(cov)
+    for (b, h), (o, rcov, st) in ref.items():
+        assert st == 0
+        got = out[b, :, h, :inp.d]
+        assert max_abs(got, o) < ATOL_MAX
+        assert mean_abs(got, o) < ATOL_MEAN
+        np.testing.assert_array_equal(cov[b, h], rcov)
+
+
+def test_sparse_attention_random_masks(torch):
+    """test_sparse_exec.cpp:24-38 random_valid_mask: anchors on block 0 and the
+    overlapping blocks, others kept with probability p; plus future bits set
+    (sparse_attention.hpp ignores them)."""
+    rng = np.random.default_rng(220)
+    inp = Inputs("gaussian", 9, 1, 1000, 4, 2)
+    q, k, v = inp.torch()
+    nq, nk, _ = sale.grid(inp.N)
+    cells = np.zeros((1, inp.Hq, nq, nk), np.uint8)
+    for h in range(inp.Hq):
+        p = 0.2 + 0.2 * h
+        for i in range(nq):
+            for j in range(nk):
+                kb, qe = 32 * j, min(64 * i + 64, inp.N)
+                future = kb >= qe
+                overl = not future and 32 * j + 32 > 64 * i
+                cells[0, h, i, j] = 1 if (j == 0 or overl or rng.random() < p) else 0
+                if future and h == 3:
+                    cells[0, h, i, j] = 1
+    words = torch.from_numpy(sale.pack_mask(cells, inp.N).view(np.int32)).cuda()
+    out, cov = sale.block_sparse_attention(q, k, v, words, coverage=True)
+    ref = _oracle_attention(inp, cells, inp.heads())
+    out, cov = _to_np(out.float()), _to_np(cov)
+    for (b, h), (o, rcov, st) in ref.items():
+        got = out[b, :, h, :inp.d]
+        assert max_abs(got, o) < ATOL_MAX
+        assert mean_abs(got, o) < ATOL_MEAN
+        np.testing.assert_array_equal(cov[b, h], rcov)
+
+
+# ------------------------------------------------------------- accounting
+
+def test_flop_count(torch):
+    inp = Inputs("sink_local", 7, 2, 1500, 4, 2)
+    q, k, _ = inp.torch()
+    qc, qs, kc, ks = sale.quantize_qk(q, k)
+    mask = sale.selection_pass(q, k, qc, qs, kc, ks, [0.004, 0.01, 0.05, 0.3])
+    counts = _to_np(sale.flop_accounting(mask, inp.N))
+    cells = sale.unpack_mask(_to_np(mask), inp.N)
+    for b in range(inp.B):
+        for h in range(inp.Hq):
+            r = O.flop_accounting(cells[b, h], inp.N)
+            assert tuple(counts[b, h]) == (r["computed"], r["skipped"], r["total"])
+
+
+# -------------------------------------------------------------- pipeline
+
+def test_prefill_matches_stages_and_host_path(torch):
+    inp = Inputs("sink_local", 7, 1, 2048, 8, 2)
+    q, k, v = inp.torch()
+    taus = [0.004] * 4 + [0.02] * 4
+    nq, nk, nw = sale.grid(inp.N)
+    mask_out = torch.empty((1, inp.Hq, nq, nw), dtype=torch.int32, device="cuda")
+    out = sale.prefill(q, k, v, taus, mask_out=mask_out)
+    qc, qs, kc, ks = sale.quantize_qk(q, k)
+    mask = sale.selection_pass(q, k, qc, qs, kc, ks, taus)
+    out2 = sale.block_sparse_attention(q, k, v, mask)
+    assert torch.equal(mask, mask_out)
+    assert torch.equal(out, out2)
+    host_out = np.empty_like(inp.q16)
+    sale.prefill_host(inp.q16, inp.k16, inp.v16, taus, host_out)
+    np.testing.assert_array_equal(host_out, _to_np(out.view(torch.int16)).view(np.uint16))
+
+
+def test_invalid_arguments(torch):
+    inp = Inputs("gaussian", 1, 1, 256, 4, 2)
+    q, k, v = inp.torch()
+    qc, qs, kc, ks = sale.quantize_qk(q, k)
+    with pytest.raises(ValueError):
+        sale.selection_pass(q, k, qc, qs, kc, ks, 0.0)
+    with pytest.raises(ValueError):
+        sale.selection_pass(q, k, qc, qs, kc, ks, 1.0)
+    cfg = sale.default_config()
+    cfg.segment_size = 0
+    with pytest.raises(ValueError):
+        sale.selection_pass(q, k, qc, qs, kc, ks, 0.004, config=cfg)
+    cfg = sale.default_config()
+    cfg.block_q = 32
+    with pytest.raises(NotImplementedError):
+        sale.selection_pass(q, k, qc, qs, kc, ks, 0.004, config=cfg)
