@@ -141,6 +141,13 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
                            const uint16_t *v, const sale_b200_shape *shape, const double *taus,
                            const sale_b200_selection_config *cfg, uint16_t *out);
 
+/* ---- instrumentation -----------------------------------------------------
+ * With timing enabled, sale_b200_prefill records CUDA events on its stream
+ * between kernels; sale_b200_stage_times waits for the last one and returns
+ * ms[5] = quantize, base mask, sink-local stats, estimator, attention. */
+int sale_b200_set_timing(sale_b200_ctx *ctx, int enable);
+int sale_b200_stage_times(sale_b200_ctx *ctx, float *ms);
+
 /* ---- synthetic workload (host, not the hot path) --------------------------
  * workloads.hpp:125-159 sink_local_head / :104-112 gaussian_head for one head
  * (kind 0 gaussian, 1 sink_local), fp32 [n][d] each, bit-identical to the
@@ -153,6 +160,11 @@ int sale_b200_workload_head_f32(int kind, uint64_t seed, int64_t n, int64_t d, i
  * planted terms. threads <= 0 means all cores. */
 int sale_b200_workload_gqa_bf16(int kind, uint64_t seed, const sale_b200_shape *shape,
                                 uint16_t *q, uint16_t *k, uint16_t *v, int threads);
+/* Same for the KV heads [kv_begin, kv_begin + shape->kv_heads) of a model with
+ * `total_kv_heads` KV heads (and their q heads): one rank's shard. */
+int sale_b200_workload_gqa_shard_bf16(int kind, uint64_t seed, const sale_b200_shape *shape,
+                                      int64_t kv_begin, uint16_t *q, uint16_t *k, uint16_t *v,
+                                      int threads);
 
 #ifdef __cplusplus
 }

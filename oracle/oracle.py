@@ -96,7 +96,7 @@ def _load_ref():
     lib.ref_workload_head.argtypes = [C.c_int, C.c_uint64, i64, i64, i64, f32p, f32p, f32p]
     lib.ref_run_pipeline.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, i64, f64p,
                                      f64p, f64p]
-    lib.ref_sale_heads.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, i64, f64p]
+    lib.ref_sale_heads.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, i64, f64p, f64p]
     return lib
 
 

@@ -247,8 +247,10 @@ int ref_run_pipeline(const float *q, const float *k, const float *v, int64_t hea
 // The reference's own parallel_for (parallel.hpp:15) over the hot-path stages
 // WITHOUT the dense baseline: quant -> selection_pass -> block_sparse_attention
 // for each head (runner.hpp:63-80), threads workers. Wall ms via *wall_ms.
+// stage_ms[3] receives the per-stage thread-time summed over heads (quant,
+// selection, computation), like runner.hpp:101-106.
 int ref_sale_heads(const float *q, const float *k, const float *v, int64_t heads, int64_t n,
-                   int64_t d, double tau, int64_t threads, double *wall_ms) {
+                   int64_t d, double tau, int64_t threads, double *wall_ms, double *stage_ms) {
     return guarded([&] {
         std::vector<HeadInput> hs;
         hs.reserve(static_cast<std::size_t>(heads));
@@ -256,16 +258,30 @@ int ref_sale_heads(const float *q, const float *k, const float *v, int64_t heads
             hs.push_back(to_head(q + h * n * d, k + h * n * d, v + h * n * d, n, d));
         SelectionConfig cfg;
         cfg.tau = tau;
-        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<double> st(static_cast<std::size_t>(3 * heads), 0.0);
+        using clk = std::chrono::steady_clock;
+        auto ms = [](clk::time_point a) {
+            return std::chrono::duration<double, std::milli>(clk::now() - a).count();
+        };
+        const auto t0 = clk::now();
         parallel_for(hs.size(), static_cast<std::size_t>(threads), [&](std::size_t h) {
             const BlockGrid grid(hs[h].seq_len(), cfg.block_q, cfg.block_k);
+            auto t = clk::now();
             const QuantizedMatrix q4 = quantize_per_token(hs[h].query);
             const QuantizedMatrix k4 = quantize_per_key_block(hs[h].key, grid);
+            st[3 * h] = ms(t);
+            t = clk::now();
             const BlockMask mask = selection_pass(hs[h], q4, k4, cfg);
+            st[3 * h + 1] = ms(t);
+            t = clk::now();
             (void)block_sparse_attention(hs[h], mask, grid);
+            st[3 * h + 2] = ms(t);
         });
-        *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
-                       .count();
+        *wall_ms = ms(t0);
+        for (int i = 0; i < 3; ++i) {
+            stage_ms[i] = 0.0;
+            for (int64_t h = 0; h < heads; ++h) stage_ms[i] += st[3 * h + i];
+        }
     });
 }
 

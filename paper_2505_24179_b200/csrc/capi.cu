@@ -37,6 +37,9 @@ struct sale_b200_ctx {
     uint8_t *io = nullptr;
     size_t io_bytes = 0;
     cudaStream_t io_stream = nullptr;
+    // optional per-stage event timing of sale_b200_prefill
+    bool timing = false;
+    cudaEvent_t ev[6] = {};
 };
 
 namespace {
@@ -60,6 +63,11 @@ int cuda_fail(sale_b200_ctx *ctx, cudaError_t e, const char *where) {
     } while (0)
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Stage boundaries: 0 start, 1 quantized, 2 base mask, 3 stats, 4 estimate, 5 attention.
+void mark(sale_b200_ctx *ctx, int i, cudaStream_t stream) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[i], stream);
+}
 
 int check_shape(sale_b200_ctx *ctx, const sale_b200_shape *s) {
     if (!s) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "shape is NULL");
@@ -244,11 +252,16 @@ int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *
     if ((st = ensure_units(ctx, s.tokens, stream))) return st;
     const float isd = inv_sqrt_dim(s.head_dim);
     SALE_CUDA(ctx, launch_base_mask(mask, s.batch, s.q_heads, s.tokens, stream));
+    mark(ctx, 2, stream);
     SALE_CUDA(ctx, launch_sink_local_stats(q, k, s.batch, s.tokens, s.q_heads, s.kv_heads, isd,
                                            ctx->d_taus, thresh, dbg ? dbg->running_max : nullptr,
                                            dbg ? dbg->exp_sum : nullptr, dbg ? dbg->bound : nullptr,
                                            stream));
-    if (ctx->n_units == 0) return SALE_B200_OK;
+    mark(ctx, 3, stream);
+    if (ctx->n_units == 0) {
+        mark(ctx, 4, stream);
+        return SALE_B200_OK;
+    }
     CUtensorMap tm_qc, tm_kc;
     if ((st = make_map(ctx, &tm_qc, q_codes, false, s.batch, s.tokens, s.q_heads, 128, 128))) return st;
     if ((st = make_map(ctx, &tm_kc, k_codes, false, s.batch, s.tokens, s.kv_heads, 128, 64))) return st;
@@ -256,6 +269,7 @@ int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *
                                    thresh, mask, s.batch, s.tokens, static_cast<int>(s.q_heads),
                                    static_cast<int>(s.kv_heads), isd,
                                    dbg ? dbg->block_max : nullptr, stream));
+    mark(ctx, 4, stream);
     return SALE_B200_OK;
 }
 
@@ -271,6 +285,7 @@ int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void 
     SALE_CUDA(ctx, launch_sparse_attention(tq, tk, tv, mask, out, coverage, s.batch, s.tokens,
                                            static_cast<int>(s.q_heads), static_cast<int>(s.kv_heads),
                                            scale_log2, stream));
+    mark(ctx, 5, stream);
     return SALE_B200_OK;
 }
 
@@ -314,9 +329,29 @@ int sale_b200_ctx_create(int device, sale_b200_ctx **out) {
     return SALE_B200_OK;
 }
 
+int sale_b200_set_timing(sale_b200_ctx *ctx, int enable) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (enable && !ctx->ev[0])
+        for (auto &e : ctx->ev) SALE_CUDA(ctx, cudaEventCreate(&e));
+    ctx->timing = enable != 0;
+    return SALE_B200_OK;
+}
+
+int sale_b200_stage_times(sale_b200_ctx *ctx, float *ms) {
+    if (!ctx || !ms) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ctx->ev[0]) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "timing was never enabled");
+    SALE_CUDA(ctx, cudaEventSynchronize(ctx->ev[5]));
+    for (int i = 0; i < 5; ++i) SALE_CUDA(ctx, cudaEventElapsedTime(&ms[i], ctx->ev[i], ctx->ev[i + 1]));
+    return SALE_B200_OK;
+}
+
 void sale_b200_ctx_destroy(sale_b200_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->d_taus) cudaFree(ctx->d_taus);
     if (ctx->d_units) cudaFree(ctx->d_units);
@@ -425,9 +460,11 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
     if ((st = ensure_workspace(ctx, *shape, &w))) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uint32_t *mask = mask_out ? mask_out : w.mask;
+    mark(ctx, 0, s);
     SALE_CUDA(ctx, launch_quantize_qk(q, k, w.q_codes, w.q_scales, w.k_codes, w.k_scales,
                                       shape->batch, shape->tokens, shape->q_heads,
                                       shape->kv_heads, s));
+    mark(ctx, 1, s);
     if ((st = select_impl(ctx, q, k, w.q_codes, w.q_scales, w.k_codes, w.k_scales, *shape, taus,
                           mask, w.thresh, nullptr, s)))
         return st;

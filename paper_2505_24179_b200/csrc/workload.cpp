@@ -166,7 +166,13 @@ int sale_b200_workload_head_f32(int kind, uint64_t seed, int64_t n, int64_t d, i
 
 int sale_b200_workload_gqa_bf16(int kind, uint64_t seed, const sale_b200_shape *shape, uint16_t *q,
                                 uint16_t *k, uint16_t *v, int threads) {
-    if (!shape || !q || !k || !v) return SALE_B200_INVALID_ARGUMENT;
+    return sale_b200_workload_gqa_shard_bf16(kind, seed, shape, 0, q, k, v, threads);
+}
+
+int sale_b200_workload_gqa_shard_bf16(int kind, uint64_t seed, const sale_b200_shape *shape,
+                                      int64_t kv_begin, uint16_t *q, uint16_t *k, uint16_t *v,
+                                      int threads) {
+    if (!shape || !q || !k || !v || kv_begin < 0) return SALE_B200_INVALID_ARGUMENT;
     const int64_t B = shape->batch, N = shape->tokens, Hq = shape->q_heads, Hkv = shape->kv_heads,
                   d = shape->head_dim;
     if (B < 1 || N < 1 || Hq < 1 || Hkv < 1 || d < 1 || d > 128 || Hq % Hkv)
@@ -177,7 +183,7 @@ int sale_b200_workload_gqa_bf16(int kind, uint64_t seed, const sale_b200_shape *
     std::vector<Planted> planted(static_cast<size_t>(B * Hkv));
     if (kind == 1)
         parallel(B * Hkv, threads, [&](int64_t t) {
-            planted[t] = planted_terms(seed + static_cast<uint64_t>(t / Hkv), t % Hkv, N, d);
+            planted[t] = planted_terms(seed + static_cast<uint64_t>(t / Hkv), kv_begin + t % Hkv, N, d);
         });
     // phase 2: Gaussian base + planted, in row chunks
     const int64_t chunk = 4096;
@@ -193,15 +199,15 @@ int sale_b200_workload_gqa_bf16(int kind, uint64_t seed, const sale_b200_shape *
         if (x < Hq) {
             const int64_t g = x / G, r = x % G;
             const Planted *pl = kind == 1 ? &planted[b * Hkv + g] : nullptr;
-            const uint64_t stream = r == 0 ? head_seed(sb, g)
-                                           : head_seed(sb, g) + kQStream * static_cast<uint64_t>(r);
+            const uint64_t hs = head_seed(sb, kv_begin + g);
+            const uint64_t stream = r == 0 ? hs : hs + kQStream * static_cast<uint64_t>(r);
             fill_rows(stream, 0, r0, r1, d, kQ, pl, nullptr, q + ((b * N) * Hq + x) * 128, Hq * 128);
         } else {
             const bool is_k = x < Hq + Hkv;
             const int64_t g = is_k ? x - Hq : x - Hq - Hkv;
             const Planted *pl = kind == 1 && is_k ? &planted[b * Hkv + g] : nullptr;
             uint16_t *dst = (is_k ? k : v) + ((b * N) * Hkv + g) * 128;
-            fill_rows(head_seed(sb, g), is_k ? nd : 2 * nd, r0, r1, d, is_k ? kK : kV, pl, nullptr,
+            fill_rows(head_seed(sb, kv_begin + g), is_k ? nd : 2 * nd, r0, r1, d, is_k ? kK : kV, pl, nullptr,
                       dst, Hkv * 128);
         }
     });

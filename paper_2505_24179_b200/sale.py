@@ -83,6 +83,10 @@ def load_library() -> C.CDLL:
         "sale_b200_workload_head_f32": (C.c_int, [C.c_int, C.c_uint64, i64, i64, i64, vp, vp, vp]),
         "sale_b200_workload_gqa_bf16": (C.c_int, [C.c_int, C.c_uint64, P(Shape), vp, vp, vp,
                                                   C.c_int]),
+        "sale_b200_workload_gqa_shard_bf16": (C.c_int, [C.c_int, C.c_uint64, P(Shape), i64, vp,
+                                                        vp, vp, C.c_int]),
+        "sale_b200_set_timing": (C.c_int, [vp, C.c_int]),
+        "sale_b200_stage_times": (C.c_int, [vp, P(C.c_float)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -327,10 +331,25 @@ def workload_head_f32(kind: str, seed: int, tokens: int, dim: int, head: int = 0
     return q, k, v
 
 
+def set_timing(enable: bool = True):
+    ctx = context()
+    ctx._check(ctx.lib.sale_b200_set_timing(ctx.handle, int(enable)))
+
+
+def stage_times():
+    """ms of the last timed prefill: quantize, base mask, stats, estimator, attention."""
+    ctx = context()
+    ms = (C.c_float * 5)()
+    ctx._check(ctx.lib.sale_b200_stage_times(ctx.handle, ms))
+    return dict(zip(("quantize", "base_mask", "stats", "estimate", "attention"), list(ms)))
+
+
 def workload_gqa(kind: str, seed: int, batch: int, tokens: int, q_heads: int, kv_heads: int,
-                 head_dim: int = 128, threads: int = 0, out=None):
+                 head_dim: int = 128, threads: int = 0, out=None, kv_begin: int = 0):
     """GQA extension of the reference generator as bf16 bit
-    patterns: uint16 q [B,N,Hq,128], k, v [B,N,Hkv,128] (numpy, host)."""
+    patterns: uint16 q [B,N,Hq,128], k, v [B,N,Hkv,128] (numpy, host).
+    kv_begin > 0 generates the shard of KV heads [kv_begin, kv_begin+kv_heads)
+    of a larger model (with their q heads)."""
     lib = load_library()
     if out is None:
         q = np.empty((batch, tokens, q_heads, HEAD_PITCH), np.uint16)
@@ -339,9 +358,9 @@ def workload_gqa(kind: str, seed: int, batch: int, tokens: int, q_heads: int, kv
     else:
         q, k, v = out
     s = Shape(batch, tokens, q_heads, kv_heads, head_dim)
-    st = lib.sale_b200_workload_gqa_bf16({"gaussian": 0, "sink_local": 1}[kind], seed,
-                                         C.byref(s), q.ctypes.data, k.ctypes.data,
-                                         v.ctypes.data, threads)
+    st = lib.sale_b200_workload_gqa_shard_bf16({"gaussian": 0, "sink_local": 1}[kind], seed,
+                                               C.byref(s), kv_begin, q.ctypes.data,
+                                               k.ctypes.data, v.ctypes.data, threads)
     if st:
         raise ValueError(f"workload_gqa: status {st}")
     return q, k, v
