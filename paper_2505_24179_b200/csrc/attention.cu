@@ -53,6 +53,23 @@ __device__ __forceinline__ uint32_t mask_bits4(const uint32_t *row, int64_t word
     return static_cast<uint32_t>(v >> sh) & 0xFu;
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ unsigned long long pack_f2(float lo, float hi) {
+    return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+// x = x * a + b on two packed fp32 lanes (FFMA2)
+__device__ __forceinline__ void ffma2_f32(unsigned long long &x, unsigned long long a,
+                                          unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void fadd2_f32(unsigned long long &x, unsigned long long a) {
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(a));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&p);
@@ -77,17 +94,22 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
     for (int c4 = 0; c4 < NK / 32; ++c4)
         tmem_ld32(sAddr + 32 * c4, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c4]));
     tmem_ld_wait();
-    // column c valid iff its 32-key sub-block is selected and c <= lim (causal)
-    float mt = -INFINITY;
-    int nvalid = 0;
+    // column c valid iff its 32-key sub-block is selected and c <= lim (causal);
+    // fully selected, fully past tiles skip the per-element test.
+    const bool full = nib == ((1u << (NK / 32)) - 1u) && lim >= NK - 1;
+    int nvalid = NK;
+    if (!full) {
+        nvalid = 0;
 #pragma unroll
-    for (int c = 0; c < NK; ++c) {
-        const bool ok = ((nib >> (c >> 5)) & 1u) && c <= lim;
-        const float v = ok ? __uint_as_float(s[c]) : -INFINITY;
-        s[c] = __float_as_uint(v);
-        mt = fmaxf(mt, v);
-        nvalid += ok ? 1 : 0;
+        for (int c = 0; c < NK; ++c) {
+            const bool ok = ((nib >> (c >> 5)) & 1u) && c <= lim;
+            s[c] = ok ? s[c] : __float_as_uint(-INFINITY);
+            nvalid += ok ? 1 : 0;
+        }
     }
+    float mt = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < NK; c += 2) mt = fmax3(mt, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
     const float m_new = fmaxf(st.m_run, mt * scale_log2);
     const bool need = st.m_run != -INFINITY && m_new > st.m_run + 8.0f;
     if (st.m_run == -INFINITY) st.m_run = m_new;
@@ -111,17 +133,22 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
             st.m_run = m_new;
         }
     }
-    const float neg_m = -st.m_run;
-    float psum = 0.0f;
+    // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
+    // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
+    const float neg_m = st.m_run == -INFINITY ? 0.0f : -st.m_run;
+    const unsigned long long sc2 = pack_f2(scale_log2, scale_log2), nm2 = pack_f2(neg_m, neg_m);
+    unsigned long long psum2 = 0ull;
 #pragma unroll
     for (int c2 = 0; c2 < NK / 2; ++c2) {
-        const float x0 = __uint_as_float(s[2 * c2]), x1 = __uint_as_float(s[2 * c2 + 1]);
-        const float p0 = x0 == -INFINITY ? 0.0f : ex2_approx(fmaf(x0, scale_log2, neg_m));
-        const float p1 = x1 == -INFINITY ? 0.0f : ex2_approx(fmaf(x1, scale_log2, neg_m));
-        psum += p0 + p1;
+        unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
+        ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
+        const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
+        const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
+        fadd2_f32(psum2, pack_f2(p0, p1));
         s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
     }
-    st.l_run += psum;
+    st.l_run += __uint_as_float(static_cast<uint32_t>(psum2)) +
+                __uint_as_float(static_cast<uint32_t>(psum2 >> 32));
     st.cov += nvalid;
     if constexpr (NK == 128) {
         tmem_st32(sAddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
@@ -148,12 +175,17 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t words = (nk + 31) / 32;
     const int n_t = static_cast<int>(nq / 2 + 1);
-    const int bh = batch * hq;
-    const int t = n_t - 1 - static_cast<int>(blockIdx.x / bh); // heaviest tiles first
-    const int rest = static_cast<int>(blockIdx.x % bh);
-    const int h = rest % hq;
-    const int b = rest / hq;
-    const int g = h / (hq / hkv);
+    // CTA order: (batch, KV head) major, then query tiles heaviest first, then
+    // the query heads of the GQA group — concurrently resident CTAs stream the
+    // same K/V prefix, so the ~64 MB of K/V per KV head at 128K is read from
+    // HBM about once and then served from L2.
+    const int group = hq / hkv;
+    const int hh = static_cast<int>(blockIdx.x % group);
+    const int t = n_t - 1 - static_cast<int>((blockIdx.x / group) % n_t);
+    const int bg = static_cast<int>(blockIdx.x / (group * n_t));
+    const int g = bg % hkv;
+    const int b = bg / hkv;
+    const int h = g * group + hh;
     const int row0 = 128 * t - 64;
     const int64_t qa = 2 * static_cast<int64_t>(t) - 1, qb = 2 * static_cast<int64_t>(t);
 

@@ -24,7 +24,8 @@
 
 namespace sale_b200 {
 
-constexpr int kSegPerUnit = 16;           // segments per work unit (2048 keys)
+constexpr int kSegPerUnit = 64;           // segments per work unit (8192 keys)
+constexpr int kSegWords = kSegPerUnit / 32;
 constexpr int kEstHeads = 4;               // query heads per CTA
 constexpr int kEstStages = 8;              // TMA ring depth
 constexpr int kStageKeys = 64;             // keys per stage (2 key blocks)
@@ -41,7 +42,7 @@ struct EstSmem {
     uint64_t tmem_full[2];
     uint64_t tmem_empty[2];
     uint32_t tmem_base;
-    uint32_t seg_bits[kEstHeads][2];
+    uint32_t seg_bits[kEstHeads][2][kSegWords];
 };
 
 static_assert(kSegPerUnit == kSegPerUnitHost, "unit size mismatch");
@@ -86,7 +87,9 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             mbar_init(&sm.tmem_full[s], 1);
             mbar_init(&sm.tmem_empty[s], 8);
         }
-        for (int hh = 0; hh < kEstHeads; ++hh) sm.seg_bits[hh][0] = sm.seg_bits[hh][1] = 0;
+        for (int hh = 0; hh < kEstHeads; ++hh)
+            for (int x = 0; x < 2; ++x)
+                for (int w = 0; w < kSegWords; ++w) sm.seg_bits[hh][x][w] = 0;
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -168,11 +171,13 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             for (int x = 0; x < 2; ++x) {
                 const int hh = x == 0 ? hA : hB;
                 if (hh >= nh) continue; // warp-uniform
+                uint32_t vv[2][16];
+                tmem_ld32_pack16(lane_addr + bb * 256 + hh * kStageKeys, vv[0]);
+                tmem_ld32_pack16(lane_addr + bb * 256 + hh * kStageKeys + 32, vv[1]);
+                tmem_ld_wait();
 #pragma unroll
                 for (int jb = 0; jb < 2; ++jb) {
-                    uint32_t v[16];
-                    tmem_ld32_pack16(lane_addr + bb * 256 + hh * kStageKeys + jb * 32, v);
-                    tmem_ld_wait();
+                    uint32_t *v = vv[jb];
 #pragma unroll
                     for (int s = 8; s > 0; s >>= 1)
 #pragma unroll
@@ -198,7 +203,8 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                     const int hh = x == 0 ? hA : hB;
                     if (hh >= nh) continue;
                     const bool any = __any_sync(0xffffffffu, flag[x]);
-                    if (lane == 0 && any) atomicOr(&sm.seg_bits[hh][quad >> 1], 1u << seg);
+                    if (lane == 0 && any)
+                        atomicOr(&sm.seg_bits[hh][quad >> 1][seg >> 5], 1u << (seg & 31));
                     flag[x] = false;
                 }
             }
@@ -207,17 +213,19 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         if (ew == 0 && lane < 2 * kEstHeads) {
             const int hh = lane >> 1, half = lane & 1;
             const int64_t qi = 2 * static_cast<int64_t>(u.m) + 1 + half;
-            uint32_t bits = sm.seg_bits[hh][half];
-            if (hh < nh && qi < nq && bits) {
+            if (hh < nh && qi < nq) {
                 uint32_t *row = mask + ((static_cast<int64_t>(b) * hq + h0 + hh) * nq + qi) * words;
-                while (bits) {
-                    const int s = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    const int64_t sg = static_cast<int64_t>(kSegPerUnit) * u.c + s;
-                    const int64_t j0 = 1 + kSegment * sg; // blocks j0 .. j0+3
-                    const uint32_t w0 = static_cast<uint32_t>(j0 >> 5), sh = j0 & 31;
-                    atomicOr(row + w0, 0xFu << sh);
-                    if (sh > 28) atomicOr(row + w0 + 1, 0xFu >> (32 - sh));
+                for (int sw = 0; sw < kSegWords; ++sw) {
+                    uint32_t bits = sm.seg_bits[hh][half][sw];
+                    while (bits) {
+                        const int s = 32 * sw + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const int64_t sg = static_cast<int64_t>(kSegPerUnit) * u.c + s;
+                        const int64_t j0 = 1 + kSegment * sg; // blocks j0 .. j0+3
+                        const uint32_t w0 = static_cast<uint32_t>(j0 >> 5), sh = j0 & 31;
+                        atomicOr(row + w0, 0xFu << sh);
+                        if (sh > 28) atomicOr(row + w0 + 1, 0xFu >> (32 - sh));
+                    }
                 }
             }
         }

@@ -12,7 +12,7 @@ struct EstUnit {
     int c;    // chunk of kSegPerUnit middle segments
     int nseg; // segments in this unit
 };
-constexpr int kSegPerUnitHost = 16;
+constexpr int kSegPerUnitHost = 64;
 
 cudaError_t launch_quantize_qk(const void *q, const void *k, int8_t *q_codes, float *q_scales,
                                int8_t *k_codes, float *k_scales, int64_t batch, int64_t tokens,

@@ -3,8 +3,9 @@
 //
 // Reproduces compute_sink_local_stats (selection.hpp:129-163) and
 // threshold_bound (selection.hpp:168-173) bit-for-bit on bf16-valued inputs:
-//   s_t   = fl32(dot_seq(q, k_t)) * inv_sqrt_d   — an FFMA chain over c = 0..d-1
-//           (bf16 x bf16 products are exact in fp32, so FFMA == MUL+ADD)
+//   s_t   = fl32(dot_seq(q, k_t)) * inv_sqrt_d   — an FMA chain over c = 0..d-1
+//           (bf16 x bf16 products are exact in fp32, so FMA == MUL+ADD); two
+//           independent chains share one packed FFMA2 (fma.rn.f32x2)
 //   m     = running max in double, in I_SL block order
 //   sum_b = sequential double sum of exp(double(s_t) - m_b) over block b
 //   l     = l * exp(m_old - m_new) + sum_b      — __dmul_rn/__dadd_rn, never fused
@@ -13,6 +14,11 @@
 // see DESIGN.md "Parity" for why that cannot flip a mask bit in practice.
 // K2b compares float estimates against fb = the smallest float >= bound, which
 // is exactly equivalent to the reference's (double)est >= bound.
+//
+// CTA = one (batch, head, query block i >= 3): 64 rows x <= 224 keys x d.
+// Q and the I_SL keys are staged as bf16 with cp.async into rows padded to
+// 264 B (66 words: 16 consecutive rows hit 16 distinct banks). ~72 KB smem,
+// two CTAs per SM.
 #include "common.cuh"
 
 #include <cfloat>
@@ -24,34 +30,38 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxSlBlocks = 7;                  // {0} U [2i-4, 2i+1]
 constexpr int kMaxKeys = kMaxSlBlocks * kBlockK; // 224
-constexpr int kKeyPitch = kMaxKeys;              // kT[c][t]
 constexpr int kRows = kBlockQ;                   // 64
+constexpr int kPitch = 132;                      // bf16 per staged row (264 B)
 
 struct StatsSmem {
     union {
         struct {
-            float qT[kHeadDim][kRows];     // 32 KB
-            float kT[kHeadDim][kKeyPitch]; // 112 KB
+            __nv_bfloat16 q[kRows][kPitch];    // 16.5 KB
+            __nv_bfloat16 k[kMaxKeys][kPitch]; // 57.75 KB
         } in;
-        double e[kRows][kMaxKeys];         // 112 KB (exp terms)
+        float logit[kRows][kMaxKeys];          // 56 KB (after the dot phase)
     } u;
-    float logit[kRows][kMaxKeys];          // 56 KB
-    double mblk[kRows][kMaxSlBlocks];      // running max after each block
-    int blk_id[kMaxSlBlocks];
+    double bmax[kRows][kMaxSlBlocks];          // block max, then running max
+    double bsum[kRows][kMaxSlBlocks];          // per-block exp sums
     int blk_len[kMaxSlBlocks];
 };
 
-__device__ __forceinline__ void bf16x8_to_f32(const uint4 &u, float *f) {
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        f[2 * i] = __uint_as_float(w[i] << 16);
-        f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-    }
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool valid) {
+    const uint32_t d = smem_u32(dst);
+    const int n = valid ? 8 : 0; // src-size 0 -> zero fill
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void ffma2(unsigned long long &acc, unsigned long long a,
+                                      unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
 }
 
 // grid: (nq - 3, heads, batch) — query blocks i >= 3 (non-empty middle).
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__restrict__ k,
                         int64_t tokens, int64_t hq, int64_t hkv, float inv_sqrt_d,
                         const double *__restrict__ taus, float *__restrict__ thresh,
@@ -66,120 +76,135 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     const int64_t g = h / (hq / hkv);
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t q0 = i * kBlockQ;
-    const int64_t qrows = (q0 + kBlockQ <= tokens) ? kBlockQ : tokens - q0;
+    const int qrows = static_cast<int>((q0 + kBlockQ <= tokens) ? kBlockQ : tokens - q0);
     const int64_t frontier = frontier_block(i, tokens, nk);
-
-    // I_SL (selection.hpp:92-123) for the default geometry: {0} U [2i-4, frontier].
+    // I_SL (selection.hpp:92-123), default geometry: slot 0 = block 0, slots
+    // 1.. = blocks 2i-4 .. frontier.
     const int nsl = static_cast<int>(1 + frontier - (2 * i - 4) + 1);
+    auto slot_token = [&](int slot) -> int64_t {
+        return slot == 0 ? 0 : (2 * i - 4 + slot - 1) * kBlockK;
+    };
     if (tid < kMaxSlBlocks) {
-        int id = -1, len = 0;
+        int len = 0;
         if (tid < nsl) {
-            id = tid == 0 ? 0 : static_cast<int>(2 * i - 4 + tid - 1);
-            const int64_t kb = static_cast<int64_t>(id) * kBlockK;
+            const int64_t kb = slot_token(tid);
             len = static_cast<int>((kb + kBlockK <= tokens) ? kBlockK : tokens - kb);
         }
-        sm.blk_id[tid] = id;
         sm.blk_len[tid] = len;
     }
 
-    // ---- stage Q (64 rows) and the <= 224 keys transposed into smem (fp32)
-    for (int idx = tid; idx < kRows * (kHeadDim / 8); idx += kThreads) {
-        const int r = idx % kRows, ch = idx / kRows;
-        float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (r < qrows) {
-            const uint4 u = __ldg(reinterpret_cast<const uint4 *>(
-                                      q + ((b * tokens + q0 + r) * hq + h) * kHeadDim) +
-                                  ch);
-            bf16x8_to_f32(u, f);
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sm.u.in.qT[ch * 8 + e][r] = f[e];
+    // ---- stage Q rows and I_SL keys (bf16) with cp.async, zero-filling
+    //      rows past the sequence end.
+    for (int idx = tid; idx < kRows * (kHeadDim / 4); idx += kThreads) {
+        const int r = idx / (kHeadDim / 4), ch = idx % (kHeadDim / 4);
+        const bool ok = r < qrows;
+        const __nv_bfloat16 *src = q + ((b * tokens + q0 + (ok ? r : 0)) * hq + h) * kHeadDim + 4 * ch;
+        cp_async8(&sm.u.in.q[r][4 * ch], src, ok);
     }
-    for (int idx = tid; idx < kMaxKeys * (kHeadDim / 8); idx += kThreads) {
-        const int t = idx % kMaxKeys, ch = idx / kMaxKeys;
-        const int slot = t / kBlockK, tt = t % kBlockK;
-        float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (slot < nsl) {
-            const int64_t tok = (slot == 0 ? 0 : (2 * i - 4 + slot - 1) * kBlockK) + tt;
-            if (tok < tokens) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4 *>(
-                                          k + ((b * tokens + tok) * hkv + g) * kHeadDim) +
-                                      ch);
-                bf16x8_to_f32(u, f);
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sm.u.in.kT[ch * 8 + e][t] = f[e];
+    for (int idx = tid; idx < kMaxKeys * (kHeadDim / 4); idx += kThreads) {
+        const int t = idx / (kHeadDim / 4), ch = idx % (kHeadDim / 4);
+        const int slot = t / kBlockK;
+        const int64_t tok = slot < nsl ? slot_token(slot) + t % kBlockK : tokens;
+        const bool ok = tok < tokens;
+        const __nv_bfloat16 *src = k + ((b * tokens + (ok ? tok : 0)) * hkv + g) * kHeadDim + 4 * ch;
+        cp_async8(&sm.u.in.k[t][4 * ch], src, ok);
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
-    // ---- fp32 logits: thread = 4 rows x 14 keys, sequential over c.
+    // ---- fp32 logits: thread = 4 rows x 14 keys (kg + 16 j), sequential over c;
+    //      key pairs (kg + 32p, kg + 32p + 16) share one FFMA2.
     {
         const int rg = tid / 16, kg = tid % 16;
-        float acc[4][14];
+        unsigned long long acc[4][7];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int j = 0; j < 14; ++j) acc[a][j] = 0.0f;
+            for (int p = 0; p < 7; ++p) acc[a][p] = 0ull;
+        const uint32_t *qw[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) qw[a] = reinterpret_cast<const uint32_t *>(sm.u.in.q[rg * 4 + a]);
+        const uint32_t *kw = reinterpret_cast<const uint32_t *>(sm.u.in.k[kg]);
+        constexpr int kRowWords = kPitch / 2;
 #pragma unroll 2
-        for (int c = 0; c < kHeadDim; ++c) {
-            const float4 qv = *reinterpret_cast<const float4 *>(&sm.u.in.qT[c][rg * 4]);
-            float kv[14];
+        for (int cw = 0; cw < kHeadDim / 2; ++cw) {
+            uint32_t qv[4], kv[14];
 #pragma unroll
-            for (int j = 0; j < 14; ++j) kv[j] = sm.u.in.kT[c][kg + 16 * j];
+            for (int a = 0; a < 4; ++a) qv[a] = qw[a][cw];
 #pragma unroll
-            for (int j = 0; j < 14; ++j) {
-                acc[0][j] = __fmaf_rn(qv.x, kv[j], acc[0][j]);
-                acc[1][j] = __fmaf_rn(qv.y, kv[j], acc[1][j]);
-                acc[2][j] = __fmaf_rn(qv.z, kv[j], acc[2][j]);
-                acc[3][j] = __fmaf_rn(qv.w, kv[j], acc[3][j]);
+            for (int j = 0; j < 14; ++j) kv[j] = kw[(16 * j) * kRowWords + cw];
+            // c = 2cw (low halves), then c = 2cw + 1 (high halves)
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                unsigned long long kp[7];
+#pragma unroll
+                for (int p = 0; p < 7; ++p) {
+                    const uint32_t x0 = half ? (kv[2 * p] & 0xFFFF0000u) : (kv[2 * p] << 16);
+                    const uint32_t x1 = half ? (kv[2 * p + 1] & 0xFFFF0000u) : (kv[2 * p + 1] << 16);
+                    kp[p] = pack2(__uint_as_float(x0), __uint_as_float(x1));
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const uint32_t y = half ? (qv[a] & 0xFFFF0000u) : (qv[a] << 16);
+                    const unsigned long long qq = pack2(__uint_as_float(y), __uint_as_float(y));
+#pragma unroll
+                    for (int p = 0; p < 7; ++p) ffma2(acc[a][p], qq, kp[p]);
+                }
             }
         }
+        __syncthreads(); // staging area becomes the logit buffer
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int j = 0; j < 14; ++j)
-                sm.logit[rg * 4 + a][kg + 16 * j] = __fmul_rn(acc[a][j], inv_sqrt_d);
+            for (int p = 0; p < 7; ++p) {
+                const float lo = __uint_as_float(static_cast<uint32_t>(acc[a][p]));
+                const float hi = __uint_as_float(static_cast<uint32_t>(acc[a][p] >> 32));
+                sm.u.logit[rg * 4 + a][kg + 32 * p] = __fmul_rn(lo, inv_sqrt_d);
+                sm.u.logit[rg * 4 + a][kg + 32 * p + 16] = __fmul_rn(hi, inv_sqrt_d);
+            }
     }
     __syncthreads();
 
-    // ---- running max per (row, block) in I_SL order
-    if (tid < kRows) {
+    // ---- (row, block) tasks: block max
+    for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
+        const int r = task / kMaxSlBlocks, s = task % kMaxSlBlocks;
+        double bm = -INFINITY;
+        if (s < nsl)
+            for (int t = 0; t < sm.blk_len[s]; ++t)
+                bm = fmax(bm, static_cast<double>(sm.u.logit[r][s * kBlockK + t]));
+        sm.bmax[r][s] = bm;
+    }
+    __syncthreads();
+    if (tid < kRows) { // running max after each block, in I_SL order
         double m = -INFINITY;
         for (int s = 0; s < nsl; ++s) {
-            double bm = -INFINITY;
-            for (int t = 0; t < sm.blk_len[s]; ++t)
-                bm = fmax(bm, static_cast<double>(sm.logit[tid][s * kBlockK + t]));
-            m = fmax(m, bm);
-            sm.mblk[tid][s] = m;
+            m = fmax(m, sm.bmax[tid][s]);
+            sm.bmax[tid][s] = m;
         }
     }
     __syncthreads();
-
-    // ---- exp terms, all threads (the u.in staging area is dead now)
-    for (int idx = tid; idx < kRows * kMaxKeys; idx += kThreads) {
-        const int r = idx / kMaxKeys, t = idx % kMaxKeys;
-        const int s = t / kBlockK;
-        double e = 0.0;
-        if (s < nsl && (t % kBlockK) < sm.blk_len[s])
-            e = exp(static_cast<double>(sm.logit[r][t]) - sm.mblk[r][s]);
-        sm.u.e[r][t] = e;
+    // ---- (row, block) tasks: sequential double sum of exp(s_t - m_new)
+    for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
+        const int r = task / kMaxSlBlocks, s = task % kMaxSlBlocks;
+        if (s >= nsl) continue;
+        const double m_new = sm.bmax[r][s];
+        double sum = 0.0;
+        for (int t = 0; t < sm.blk_len[s]; ++t)
+            sum = __dadd_rn(sum, exp(static_cast<double>(sm.u.logit[r][s * kBlockK + t]) - m_new));
+        sm.bsum[r][s] = sum;
     }
     __syncthreads();
 
-    // ---- sequential combination per row + bound
+    // ---- per row: l = l * exp(m_old - m_new) + sum_b, then the bound
     if (tid < qrows) {
         const int r = tid;
         double l = 0.0, m_old = -INFINITY;
         for (int s = 0; s < nsl; ++s) {
-            const double m_new = sm.mblk[r][s];
-            double sum = 0.0;
-            for (int t = 0; t < sm.blk_len[s]; ++t) sum = __dadd_rn(sum, sm.u.e[r][s * kBlockK + t]);
-            l = __dadd_rn(__dmul_rn(l, exp(m_old - m_new)), sum);
+            const double m_new = sm.bmax[r][s];
+            l = __dadd_rn(__dmul_rn(l, exp(m_old - m_new)), sm.bsum[r][s]);
             m_old = m_new;
         }
-        const double tau = taus[h];
-        double scaled = __dmul_rn(tau, l);
+        double scaled = __dmul_rn(taus[h], l);
         if (scaled < DBL_MIN) scaled = DBL_MIN;
         const double bound = __dadd_rn(m_old, log(scaled));
         const int64_t o = (b * hq + h) * tokens + q0 + r;
