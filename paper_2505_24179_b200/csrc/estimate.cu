@@ -31,7 +31,8 @@ constexpr int kEstStages = 8;              // TMA ring depth
 constexpr int kStageKeys = 64;             // keys per stage (2 key blocks)
 constexpr int kATileBytes = 128 * kHeadDim;        // 16 KB per head
 constexpr int kBStageBytes = kStageKeys * kHeadDim; // 8 KB
-constexpr int kEstThreads = 384;           // warps 0-3 control, 4-11 epilogue
+constexpr int kEpiWarps = 16;             // one (lane quadrant, query head) per warp
+constexpr int kEstThreads = 128 + 32 * kEpiWarps; // warps 0-3 control, 4-19 epilogue
 
 struct EstSmem {
     alignas(1024) uint8_t a[kEstHeads][kATileBytes];
@@ -85,7 +86,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         mbar_init(&sm.a_full, 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.tmem_full[s], 1);
-            mbar_init(&sm.tmem_empty[s], 8);
+            mbar_init(&sm.tmem_empty[s], kEpiWarps);
         }
         for (int hh = 0; hh < kEstHeads; ++hh)
             for (int x = 0; x < 2; ++x)
@@ -145,32 +146,24 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const int r = quad * 32 + lane;       // row within the 128-row tile
         const int64_t tok = row0 + r;
         const bool row_ok = tok < tokens;
-        const int hA = ew >> 2, hB = hA + 2;  // this warp's two heads
-        float qs[2], fb[2];
-        bool flag[2] = {false, false};
-#pragma unroll
-        for (int x = 0; x < 2; ++x) {
-            const int hh = x == 0 ? hA : hB;
-            qs[x] = 0.0f;
-            fb[x] = INFINITY;
-            if (row_ok && hh < nh) {
-                const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
-                qs[x] = q_scales[o];
-                fb[x] = thresh[o];
-            }
+        const int hh = ew >> 2;               // this warp's query head (0..3)
+        const bool active = hh < nh;          // warp-uniform
+        float qs = 0.0f, fb = INFINITY;
+        bool flag = false;
+        if (row_ok && active) {
+            const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
+            qs = q_scales[o];
+            fb = thresh[o];
         }
         const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        const float *ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
         for (int k = 0; k < nstages; ++k) {
             const int bb = k & 1;
             const int64_t jb0 = (key_base + kStageKeys * k) / kBlockK;
-            const float* ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
             const float ks0 = ks_row[jb0], ks1 = ks_row[jb0 + 1];
             mbar_wait(&sm.tmem_full[bb], (k >> 1) & 1);
             tc_fence_after();
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-                const int hh = x == 0 ? hA : hB;
-                if (hh >= nh) continue; // warp-uniform
+            if (active) {
                 uint32_t vv[2][16];
                 tmem_ld32_pack16(lane_addr + bb * 256 + hh * kStageKeys, vv[0]);
                 tmem_ld32_pack16(lane_addr + bb * 256 + hh * kStageKeys + 32, vv[1]);
@@ -185,9 +178,9 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                     const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
                     const int hi = static_cast<int16_t>(v[0] >> 16);
                     const int mx = lo > hi ? lo : hi;
-                    const float rs = __fmul_rn(__fmul_rn(qs[x], jb ? ks1 : ks0), inv_sqrt_d);
+                    const float rs = __fmul_rn(__fmul_rn(qs, jb ? ks1 : ks0), inv_sqrt_d);
                     const float est = __fmul_rn(rs, static_cast<float>(mx));
-                    flag[x] |= est >= fb[x];
+                    flag |= est >= fb;
                     if (dbg_max != nullptr && row_ok)
                         dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
                                 jb0 + jb] = mx;
@@ -196,20 +189,15 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.tmem_empty[bb]);
-            if (k & 1) {
+            if ((k & 1) && active) {
                 const int seg = k >> 1;
-#pragma unroll
-                for (int x = 0; x < 2; ++x) {
-                    const int hh = x == 0 ? hA : hB;
-                    if (hh >= nh) continue;
-                    const bool any = __any_sync(0xffffffffu, flag[x]);
-                    if (lane == 0 && any)
-                        atomicOr(&sm.seg_bits[hh][quad >> 1][seg >> 5], 1u << (seg & 31));
-                    flag[x] = false;
-                }
+                const bool any = __any_sync(0xffffffffu, flag);
+                if (lane == 0 && any)
+                    atomicOr(&sm.seg_bits[hh][quad >> 1][seg >> 5], 1u << (seg & 31));
+                flag = false;
             }
         }
-        named_bar_sync(1, 256);
+        named_bar_sync(1, 32 * kEpiWarps);
         if (ew == 0 && lane < 2 * kEstHeads) {
             const int hh = lane >> 1, half = lane & 1;
             const int64_t qi = 2 * static_cast<int64_t>(u.m) + 1 + half;

@@ -39,7 +39,7 @@ struct StatsSmem {
             __nv_bfloat16 q[kRows][kPitch];    // 16.5 KB
             __nv_bfloat16 k[kMaxKeys][kPitch]; // 57.75 KB
         } in;
-        float logit[kRows][kMaxKeys];          // 56 KB (after the dot phase)
+        float logit[kRows][kMaxKeys + 1];      // 56 KB (after the dot phase), padded
     } u;
     double bmax[kRows][kMaxSlBlocks];          // block max, then running max
     double bsum[kRows][kMaxSlBlocks];          // per-block exp sums
@@ -167,7 +167,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
 
     // ---- (row, block) tasks: block max
     for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
-        const int r = task / kMaxSlBlocks, s = task % kMaxSlBlocks;
+        const int r = task % kRows, s = task / kRows; // lanes = rows: conflict-free
         double bm = -INFINITY;
         if (s < nsl)
             for (int t = 0; t < sm.blk_len[s]; ++t)
@@ -185,7 +185,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     __syncthreads();
     // ---- (row, block) tasks: sequential double sum of exp(s_t - m_new)
     for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
-        const int r = task / kMaxSlBlocks, s = task % kMaxSlBlocks;
+        const int r = task % kRows, s = task / kRows;
         if (s >= nsl) continue;
         const double m_new = sm.bmax[r][s];
         double sum = 0.0;

@@ -41,7 +41,12 @@ for tau in (0.004, 0.016, 0.064):
     pair_tiles = pa.sum()
     single = seg.sum()  # tiles if every q-block had its own M=64 tile
     dense_pairs = sum(((np.where(np.arange(ns + 1) == 0, 0, 32 + 128 * (np.arange(ns + 1) - 1)) < 64 * (min(2 * t, nq - 1) + 1)).sum()) for t in range(T)) * 32
+    # pairing across heads of a GQA group: (h, h+1) at the same q-block
+    hp = (seg[0::2] | seg[1::2]).sum()
+    # four heads of a group at the same q-block (M=256 as 2x128 pairs, union)
+    h4 = (seg[0::4] | seg[1::4] | seg[2::4] | seg[3::4]).sum()
     print(f"N={N} tau={tau}: block density {dens:.4f}; segment-tile density (per q-block) "
           f"{single / (seg_causal.sum() * 32):.4f}; 128-row pair tiles {pair_tiles} = "
-          f"{pair_tiles / dense_pairs:.4f} of dense pair tiles; pair overhead "
-          f"{2 * pair_tiles / single:.3f}x")
+          f"{pair_tiles / dense_pairs:.4f} of dense pair tiles; q-block-pair overhead "
+          f"{2 * pair_tiles / single:.3f}x; head-pair overhead {2 * hp / single:.3f}x; "
+          f"4-head union overhead {4 * h4 / single:.3f}x")
