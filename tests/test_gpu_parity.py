@@ -29,6 +29,37 @@ def _to_np(t):
     return t.detach().cpu().numpy()
 
 
+# ------------------------------------------------------ golden (reference)
+
+def test_golden_reference_fixture(torch):
+    """tests/golden/ref_gqa_640.npz was produced by the unmodified reference
+    (tests/golden/make_golden.py); no oracle involved."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_gqa_640.npz"))
+    t = lambda a: torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).cuda()
+    q, k, v = t(g["q16"]), t(g["k16"]), t(g["v16"])
+    N = q.shape[1]
+    qc, qs, kc, ks = (_to_np(x) for x in sale.quantize_qk(q, k))
+    np.testing.assert_array_equal(kc[0, :, 0], g["k_codes"])
+    np.testing.assert_array_equal(ks[0, 0], g["k_scales"])
+    qct, qst, kct, kst = sale.quantize_qk(q, k)
+    for tau in (0.004, 0.05):
+        mask = sale.selection_pass(q, k, qct, qst, kct, kst, tau)
+        cells = sale.unpack_mask(_to_np(mask), N)
+        for h in range(q.shape[2]):
+            np.testing.assert_array_equal(cells[0, h], g[f"mask_{h}_{tau}"])
+    mask = sale.selection_pass(q, k, qct, qst, kct, kst, 0.004)
+    out, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True)
+    full = sale.full_attention(q, k, v)
+    out, cov, full = _to_np(out.float()), _to_np(cov), _to_np(full.float())
+    for h in range(q.shape[2]):
+        np.testing.assert_array_equal(qc[0, :, h], g[f"q_codes_{h}"])
+        np.testing.assert_array_equal(qs[0, h], g[f"q_scales_{h}"])
+        np.testing.assert_array_equal(cov[0, h], g[f"coverage_{h}"])
+        for got, ref in ((out[0, :, h], g[f"sparse_out_{h}"]), (full[0, :, h], g[f"full_out_{h}"])):
+            assert max_abs(got, ref) < ATOL_MAX and mean_abs(got, ref) < ATOL_MEAN
+
+
 # ------------------------------------------------------------------ stage 1
 
 @pytest.mark.parametrize("kind,N,Hq,Hkv,d", [("sink_local", 1000, 4, 2, 128),
