@@ -8,34 +8,44 @@
 // t contributes to row g iff t <= g and mask(qblock(g), kblock(t)) is set;
 // fully-future mask bits are ignored; coverage[g] counts the attended tokens.
 //
-// CTA = one (batch, head) x 128-row query tile = query blocks (2t-1, 2t), rows
-// [128t-64, 128t+64). Key tiles follow the segment grid of the Selection-Pass:
-// tile 0 = the 32-key sink block, tile s+1 = keys [32+128s, 160+128s) = key
-// blocks 1+4s..4+4s. A tile is visited iff any of its 8 (qblock, kblock) bits is
-// set; inside a visited tile unselected 32-key sub-blocks and the causal
-// diagonal are masked per row.
+// CTA = one query block i (64 tokens) of TWO query heads of the same GQA group
+// (rows 0-63 head 2p, rows 64-127 head 2p+1): both halves need exactly the same
+// K/V and the same causal extent, and per-head masks of one query block
+// overlap more than masks of adjacent query blocks (profiles/mask_stats.py).
+// Key tiles follow the segment grid of the Selection-Pass: tile 0 = the
+// 32-key sink block, tile s+1 = keys [32+128s, 160+128s) = key blocks
+// 1+4s..4+4s. A tile is visited iff any of its 8 (head, kblock) bits is set;
+// inside a visited tile unselected 32-key sub-blocks and the causal diagonal
+// are masked per row.
+//
+// TMEM (512 columns): O [0,128) | S0 [128,256) | S1 [256,384) | Q [384,448).
+// Q sits in TMEM as the A operand of S = Q K^T (only K streams from shared
+// memory; with A in SMEM an M=N=128 bf16 MMA needs the full 128 B/clk port),
+// and P overwrites S in place as the A operand of O += P V.
 //
 // Pipeline (warp-specialised, one elected thread per role):
-//   warp 0  TMA: Q once, then K_j, V_j into a 2-stage ring (SW128 tiles)
+//   warp 0  TMA: K_j, V_j into a 3-stage ring (SW128 tiles)
 //   warp 1  MMA: S_j = Q K_j^T into TMEM buffer j%2 (8 x K=16), then
-//           O += P_{j-1} V_{j-1} with P read straight from TMEM (A operand)
-//   warps 4-7  softmax, thread = row: tcgen05.ld S row, mask, lazy-rescaled
-//           online softmax in the exp2 domain (O rescaled in TMEM only when
-//           the running max grows by > 8), P -> bf16 -> tcgen05.st over S.
+//           O += P_{j-1} V_{j-1}
+//   warps 4-7  softmax, thread = row: Q row -> TMEM once; per tile tcgen05.ld S
+//           row, mask, lazy-rescaled online softmax in the exp2 domain (O
+//           rescaled in TMEM only when the running max grows by > 8),
+//           P -> bf16 -> tcgen05.st over S.
 #include "common.cuh"
 
 namespace sale_b200 {
 
 constexpr int kAttnThreads = 256;
-constexpr int kMaxTiles = 4200;           // supports N <= 512K
+constexpr int kMaxTiles = 4200;                // supports N <= 512K
+constexpr int kKvStages = 3;
 constexpr int kTileBytesHalf = 128 * 64 * 2;   // 128 rows x 64 bf16 = 16 KB
-constexpr uint32_t kColO = 0, kColS0 = 128;    // TMEM: O | S0 | S1
+constexpr uint32_t kColO = 0, kColS0 = 128, kColQ = 384;
 
 struct AttnSmem {
-    alignas(1024) uint8_t q[2][kTileBytesHalf];
-    alignas(1024) uint8_t k[2][2][kTileBytesHalf];
-    alignas(1024) uint8_t v[2][2][kTileBytesHalf];
-    uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[2], p_full[2], pv_done[2];
+    alignas(1024) uint8_t k[kKvStages][2][kTileBytesHalf];
+    alignas(1024) uint8_t v[kKvStages][2][kTileBytesHalf];
+    uint64_t q_ready, k_full[kKvStages], v_full[kKvStages], kv_empty[kKvStages];
+    uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
     int ntiles;
     int warp_cnt[8];
@@ -160,10 +170,10 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
 }
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
-sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const uint32_t *__restrict__ mask,
                         __nv_bfloat16 *__restrict__ out, int32_t *__restrict__ coverage,
-                        int64_t tokens, int hq, int hkv, int batch, float scale_log2) {
+                        int64_t tokens, int hq, int hkv, float scale_log2) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     AttnSmem &sm = *reinterpret_cast<AttnSmem *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -174,27 +184,30 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t words = (nk + 31) / 32;
-    const int n_t = static_cast<int>(nq / 2 + 1);
-    // CTA order: (batch, KV head) major, then query tiles heaviest first, then
-    // the query heads of the GQA group — concurrently resident CTAs stream the
+    // CTA order: (batch, KV head) major, then query blocks heaviest first, then
+    // the head pairs of the GQA group — concurrently resident CTAs stream the
     // same K/V prefix, so the ~64 MB of K/V per KV head at 128K is read from
     // HBM about once and then served from L2.
     const int group = hq / hkv;
-    const int hh = static_cast<int>(blockIdx.x % group);
-    const int t = n_t - 1 - static_cast<int>((blockIdx.x / group) % n_t);
-    const int bg = static_cast<int>(blockIdx.x / (group * n_t));
+    const int npairs = (group + 1) / 2;
+    const int p = static_cast<int>(blockIdx.x % npairs);
+    const int64_t i = nq - 1 - static_cast<int64_t>((blockIdx.x / npairs) % nq);
+    const int bg = static_cast<int>(blockIdx.x / (npairs * nq));
     const int g = bg % hkv;
     const int b = bg / hkv;
-    const int h = g * group + hh;
-    const int row0 = 128 * t - 64;
-    const int64_t qa = 2 * static_cast<int64_t>(t) - 1, qb = 2 * static_cast<int64_t>(t);
+    const int hA = g * group + 2 * p;
+    const bool hasB = 2 * p + 1 < group;
+    const int64_t q0 = i * kBlockQ;
+    const int64_t qend = q0 + kBlockQ < tokens ? q0 + kBlockQ : tokens;
 
     if (tid == 0) {
-        mbar_init(&sm.q_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        mbar_init(&sm.q_ready, 4);
+        for (int s = 0; s < kKvStages; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.v_full[s], 1);
             mbar_init(&sm.kv_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.s_full[s], 1);
             mbar_init(&sm.p_full[s], 4);
             mbar_init(&sm.pv_done[s], 1);
@@ -205,33 +218,23 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
     if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
 
     // ---- active tile list (block-wide stream compaction, ascending order)
-    const uint32_t *rowA = (mask && qa >= 0) ? mask + ((static_cast<int64_t>(b) * hq + h) * nq + qa) * words : nullptr;
-    const uint32_t *rowB = (mask && qb < nq) ? mask + ((static_cast<int64_t>(b) * hq + h) * nq + qb) * words : nullptr;
-    const int total = t + 2;
+    const int64_t rowbase = (static_cast<int64_t>(b) * hq + hA) * nq + i;
+    const uint32_t *rowA = mask ? mask + rowbase * words : nullptr;
+    const uint32_t *rowB = (mask && hasB) ? mask + (rowbase + nq) * words : nullptr;
+    const int total = qend > kBlockK ? 1 + static_cast<int>((qend - kBlockK + 127) / 128) : 1;
     __syncthreads();
     for (int start = 0; start < total; start += kAttnThreads) {
         const int j = start + tid;
         uint32_t bits = 0;
         if (j < total) {
-            const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
-            if (key0 < tokens) {
-                const int64_t j0 = j == 0 ? 0 : 1 + 4LL * (j - 1);
-                const int nsub = j == 0 ? 1 : 4;
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const int64_t qi = half == 0 ? qa : qb;
-                    if (qi < 0 || qi >= nq) continue;
-                    const uint32_t *row = half == 0 ? rowA : rowB;
-                    uint32_t nib = mask ? mask_bits4(row, words, j0) : 0xFu;
-                    nib &= (1u << nsub) - 1u;
-                    // drop fully-future and out-of-range key blocks
-                    for (int e = 0; e < nsub; ++e) {
-                        const int64_t jb = j0 + e;
-                        if (jb >= nk || jb * kBlockK >= (qi + 1) * kBlockQ) nib &= ~(1u << e);
-                    }
-                    bits |= nib << (4 * half);
-                }
-            }
+            const int64_t j0 = j == 0 ? 0 : 1 + 4LL * (j - 1);
+            const int nsub = j == 0 ? 1 : 4;
+            uint32_t causal = 0; // key blocks that exist and are not fully future
+            for (int e = 0; e < nsub; ++e)
+                if (j0 + e < nk && (j0 + e) * kBlockK < qend) causal |= 1u << e;
+            const uint32_t nibA = mask ? mask_bits4(rowA, words, j0) : 0xFu;
+            const uint32_t nibB = !hasB ? 0u : (mask ? mask_bits4(rowB, words, j0) : 0xFu);
+            bits = (nibA & causal) | ((nibB & causal) << 4);
         }
         const bool active = bits != 0;
         const uint32_t ballot = __ballot_sync(0xffffffffu, active);
@@ -260,17 +263,13 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA
         if (elect_one() && ntiles > 0) {
-            tma_prefetch(&tm_q);
             tma_prefetch(&tm_k);
             tma_prefetch(&tm_v);
-            mbar_expect_tx(&sm.q_full, 2 * kTileBytesHalf);
-            tma_load_4d(sm.q[0], &tm_q, &sm.q_full, 0, h, row0, b);
-            tma_load_4d(sm.q[1], &tm_q, &sm.q_full, 64, h, row0, b);
             for (int jj = 0; jj < ntiles; ++jj) {
-                const int st = jj & 1;
+                const int st = jj % kKvStages;
                 const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
                 const int key0 = j == 0 ? 0 : kBlockK + 128 * (j - 1);
-                mbar_wait(&sm.kv_empty[st], ((jj >> 1) & 1) ^ 1);
+                mbar_wait(&sm.kv_empty[st], ((jj / kKvStages) & 1) ^ 1);
                 mbar_expect_tx(&sm.k_full[st], 2 * kTileBytesHalf);
                 tma_load_4d(sm.k[st][0], &tm_k, &sm.k_full[st], 0, g, key0, b);
                 tma_load_4d(sm.k[st][1], &tm_k, &sm.k_full[st], 64, g, key0, b);
@@ -283,43 +282,42 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
         // ---------------------------------------------------------------- MMA
         if (elect_one() && ntiles > 0) {
             constexpr uint32_t idesc_pv = idesc_bf16(128, 128, true);
-            const uint64_t qdesc0 = umma_desc_sw128(smem_u32(sm.q[0]), 16, 1024);
-            const uint64_t qdesc1 = umma_desc_sw128(smem_u32(sm.q[1]), 16, 1024);
-            mbar_wait(&sm.q_full, 0);
+            mbar_wait(&sm.q_ready, 0);
             tc_fence_after();
             for (int jj = 0; jj <= ntiles; ++jj) {
                 if (jj < ntiles) {
-                    const int st = jj & 1;
+                    const int st = jj % kKvStages;
+                    const int sb = jj & 1;
                     const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
                     const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
-                    mbar_wait(&sm.k_full[st], (jj >> 1) & 1);
+                    mbar_wait(&sm.k_full[st], (jj / kKvStages) & 1);
                     tc_fence_after();
                     const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
                     const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
-                    const uint32_t dS = tmem + kColS0 + 128u * static_cast<uint32_t>(st);
+                    const uint32_t dS = tmem + kColS0 + 128u * static_cast<uint32_t>(sb);
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const uint64_t a = (kk < 4 ? qdesc0 : qdesc1) + 2 * (kk & 3);
+                    for (int kk = 0; kk < 8; ++kk) { // K = 16 bf16 = 8 TMEM columns of Q
                         const uint64_t bd = (kk < 4 ? kd0 : kd1) + 2 * (kk & 3);
-                        mma_bf16_ss(dS, a, bd, idesc_s, kk > 0);
+                        mma_bf16_ts(dS, tmem + kColQ + 8 * kk, bd, idesc_s, kk > 0);
                     }
-                    tc_commit(&sm.s_full[st]);
+                    tc_commit(&sm.s_full[sb]);
                 }
                 if (jj > 0) {
-                    const int p = jj - 1;
-                    const int pst = p & 1;
-                    const int jp = static_cast<int>(sm.tiles[p] & 0xFFFFu);
+                    const int pj = jj - 1;
+                    const int pst = pj % kKvStages;
+                    const int psb = pj & 1;
+                    const int jp = static_cast<int>(sm.tiles[pj] & 0xFFFFu);
                     const int steps = jp == 0 ? 2 : 8;
-                    mbar_wait(&sm.p_full[pst], (p >> 1) & 1);
-                    mbar_wait(&sm.v_full[pst], (p >> 1) & 1);
+                    mbar_wait(&sm.p_full[psb], (pj >> 1) & 1);
+                    mbar_wait(&sm.v_full[pst], (pj / kKvStages) & 1);
                     tc_fence_after();
                     const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
-                    const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(pst);
+                    const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(psb);
                     for (int kk = 0; kk < steps; ++kk)
                         mma_bf16_ts(tmem + kColO, aP + 8 * kk, vd + 128 * kk, // +16 keys = 2 KB
-                                    idesc_pv, (p > 0 || kk > 0) ? 1u : 0u);
+                                    idesc_pv, (pj > 0 || kk > 0) ? 1u : 0u);
                     tc_commit(&sm.kv_empty[pst]);
-                    tc_commit(&sm.pv_done[pst]);
+                    tc_commit(&sm.pv_done[psb]);
                 }
             }
         }
@@ -327,10 +325,30 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
         // ------------------------------------------------------------ softmax
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
-        const int64_t grow = static_cast<int64_t>(row0) + r;
-        const bool row_ok = grow >= 0 && grow < tokens;
-        const int half = r >> 6;
+        const int half = r >> 6;                 // 0: head hA, 1: head hA + 1
+        const int h = hA + half;
+        const int64_t grow = q0 + (r & 63);
+        const bool row_ok = grow < tokens && (half == 0 || hasB);
         const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        // Q row -> TMEM columns [kColQ, kColQ + 64): the A operand of S = Q K^T
+        {
+            uint32_t a[32];
+            const uint4 *src = reinterpret_cast<const uint4 *>(
+                q + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint4 w = row_ok ? __ldg(src + 8 * hf + e) : make_uint4(0, 0, 0, 0);
+                    a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
+                }
+                tmem_st32(lane_addr + kColQ + 32 * hf, a);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.q_ready);
+        }
         SoftmaxState st;
         for (int jj = 0; jj < ntiles; ++jj) {
             const int sb = jj & 1;
@@ -360,7 +378,7 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
             tc_fence_after();
         }
         const float inv_l = st.l_run > 0.0f ? 1.0f / st.l_run : 0.0f;
-        __nv_bfloat16 *dst = row_ok ? out + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim : nullptr;
+        __nv_bfloat16 *dst = out + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim;
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
             uint32_t o[32];
@@ -396,12 +414,12 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
 
 size_t attention_smem_bytes() { return sizeof(AttnSmem) + 1024; }
 
-cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &tm_k,
-                                    const CUtensorMap &tm_v, const uint32_t *mask, void *out,
-                                    int32_t *coverage, int64_t batch, int64_t tokens, int hq,
-                                    int hkv, float scale_log2, cudaStream_t stream) {
+cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
+                                    const uint32_t *mask, void *out, int32_t *coverage,
+                                    int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
+                                    cudaStream_t stream) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
-    if (nq / 2 + 1 > kMaxTiles - 2) return cudaErrorInvalidValue;
+    if (nq / 2 + 3 > kMaxTiles) return cudaErrorInvalidValue;
     static bool configured = false;
     const size_t smem = attention_smem_bytes();
     if (!configured) {
@@ -411,10 +429,11 @@ cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    const int64_t grid = (nq / 2 + 1) * batch * hq;
+    const int npairs = (hq / hkv + 1) / 2;
+    const int64_t grid = batch * hkv * npairs * nq;
     sparse_attention_kernel<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
-        tm_q, tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out), coverage, tokens, hq, hkv,
-        static_cast<int>(batch), scale_log2);
+        static_cast<const __nv_bfloat16 *>(q), tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out),
+        coverage, tokens, hq, hkv, scale_log2);
     return cudaGetLastError();
 }
 
