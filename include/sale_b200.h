@@ -141,6 +141,15 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
                            const uint16_t *v, const sale_b200_shape *shape, const double *taus,
                            const sale_b200_selection_config *cfg, uint16_t *out);
 
+/* ---- device memory helpers (so host code needs no CUDA headers) -----------
+ * Synchronous allocation / copies on ctx's device. */
+int sale_b200_device_alloc(sale_b200_ctx *ctx, uint64_t bytes, void **out);
+int sale_b200_device_free(sale_b200_ctx *ctx, void *ptr);
+int sale_b200_copy_to_device(sale_b200_ctx *ctx, void *dst, const void *src, uint64_t bytes);
+int sale_b200_copy_to_host(sale_b200_ctx *ctx, void *dst, const void *src, uint64_t bytes);
+int sale_b200_memset(sale_b200_ctx *ctx, void *dst, int value, uint64_t bytes);
+int sale_b200_synchronize(sale_b200_ctx *ctx);
+
 /* ---- instrumentation -----------------------------------------------------
  * With timing enabled, sale_b200_prefill records CUDA events on its stream
  * between kernels; sale_b200_stage_times waits for the last one and returns

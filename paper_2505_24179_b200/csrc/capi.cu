@@ -327,6 +327,43 @@ int sale_b200_ctx_create(int device, sale_b200_ctx **out) {
     return SALE_B200_OK;
 }
 
+int sale_b200_device_alloc(sale_b200_ctx *ctx, uint64_t bytes, void **out) {
+    if (!ctx || !out) return SALE_B200_INVALID_ARGUMENT;
+    SALE_CUDA(ctx, cudaSetDevice(ctx->device));
+    SALE_CUDA(ctx, cudaMalloc(out, bytes ? bytes : 1));
+    return SALE_B200_OK;
+}
+
+int sale_b200_device_free(sale_b200_ctx *ctx, void *ptr) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    if (ptr) SALE_CUDA(ctx, cudaFree(ptr));
+    return SALE_B200_OK;
+}
+
+int sale_b200_copy_to_device(sale_b200_ctx *ctx, void *dst, const void *src, uint64_t bytes) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    SALE_CUDA(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return SALE_B200_OK;
+}
+
+int sale_b200_copy_to_host(sale_b200_ctx *ctx, void *dst, const void *src, uint64_t bytes) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    SALE_CUDA(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return SALE_B200_OK;
+}
+
+int sale_b200_memset(sale_b200_ctx *ctx, void *dst, int value, uint64_t bytes) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    SALE_CUDA(ctx, cudaMemset(dst, value, bytes));
+    return SALE_B200_OK;
+}
+
+int sale_b200_synchronize(sale_b200_ctx *ctx) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    SALE_CUDA(ctx, cudaDeviceSynchronize());
+    return SALE_B200_OK;
+}
+
 int sale_b200_set_timing(sale_b200_ctx *ctx, int enable) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);

@@ -1,0 +1,133 @@
+// test_shim.cpp — the C++ drop-in (include/sale_b200.hpp) exercised like the
+// reference's own doctest suites (proj/tests/test_quant.cpp,
+// test_selection.cpp, test_sparse_exec.cpp), comparing sale::b200::X with the
+// reference sale::X on identical bf16-valued inputs. Built by tests/cpp/Makefile
+// against the reference headers; run on a B200 by tests/test_gpu_shim.py.
+#include <sale/attention.hpp>
+#include <sale/block_grid.hpp>
+#include <sale/quant.hpp>
+#include <sale/selection.hpp>
+#include <sale/sparse_attention.hpp>
+#include <sale/workloads.hpp>
+
+#include "sale_b200.hpp"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+using namespace sale;
+
+static int failures = 0;
+#define CHECK(cond)                                                                                \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            ++failures;                                                                            \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);                            \
+        }                                                                                          \
+    } while (0)
+#define CHECK_THROWS_AS(expr, exc)                                                                 \
+    do {                                                                                           \
+        bool ok_ = false;                                                                          \
+        try {                                                                                      \
+            (void)(expr);                                                                          \
+        } catch (const exc &) {                                                                    \
+            ok_ = true;                                                                            \
+        } catch (...) {                                                                            \
+        }                                                                                          \
+        CHECK(ok_ && #exc);                                                                        \
+    } while (0)
+
+static float bf16_round(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    u &= 0xFFFF0000u;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+static HeadInput bf16_head(HeadInput h) {
+    for (DenseMatrix *m : {&h.query, &h.key, &h.value})
+        for (float &x : m->data()) x = bf16_round(x);
+    return h;
+}
+
+static HeadInput sink_head(uint64_t seed, std::size_t n, std::size_t d) {
+    WorkloadSpec spec;
+    spec.seed = seed;
+    spec.tokens = n;
+    spec.head_dim = d;
+    spec.kind = WorkloadKind::SinkLocal;
+    return bf16_head(sink_local_workload(spec).front());
+}
+
+static double max_abs_diff(const DenseMatrix &a, const DenseMatrix &b, double *mean) {
+    double worst = 0.0, sum = 0.0;
+    for (std::size_t i = 0; i < a.data().size(); ++i) {
+        const double e = std::fabs(static_cast<double>(a.data()[i]) - b.data()[i]);
+        worst = std::max(worst, e);
+        sum += e;
+    }
+    *mean = sum / static_cast<double>(a.data().size());
+    return worst;
+}
+
+int main() {
+    // test_quant.cpp:16-33 — hand rows
+    {
+        const DenseMatrix m = DenseMatrix::from_data(1, 4, {7.0f, -7.0f, 3.5f, 0.0f});
+        const QuantizedMatrix q = b200::quantize_per_token(m);
+        CHECK(q.group_scale(0) == 1.0f);
+        CHECK(q.code(0, 0) == 7 && q.code(0, 1) == -7 && q.code(0, 2) == 4 && q.code(0, 3) == 0);
+        const QuantizedMatrix z = b200::quantize_per_token(DenseMatrix(1, 4));
+        CHECK(z.group_scale(0) == 1.0f && z.code(0, 2) == 0);
+    }
+    // quantization, selection and attention against the reference
+    const std::size_t shapes[][2] = {{640, 128}, {1000, 64}, {300, 32}, {2048, 128}};
+    for (const auto &sh : shapes) {
+        const std::size_t n = sh[0], d = sh[1];
+        const HeadInput in = sink_head(70 + n, n, d);
+        const BlockGrid grid(n, 64, 32);
+        const QuantizedMatrix q4 = quantize_per_token(in.query);
+        const QuantizedMatrix k4 = quantize_per_key_block(in.key, grid);
+        CHECK(b200::quantize_per_token(in.query) == q4);
+        CHECK(b200::quantize_per_key_block(in.key, grid) == k4);
+        for (double tau : {0.004, 0.05, 1e-9}) {
+            SelectionConfig cfg;
+            cfg.tau = tau;
+            const BlockMask ref = selection_pass(in, q4, k4, cfg);
+            const BlockMask got = b200::selection_pass(in, q4, k4, cfg);
+            CHECK(got == ref);
+            const FlopCounts fr = flop_accounting(ref, grid), fg = b200::flop_accounting(got, grid);
+            CHECK(fr.computed_blocks == fg.computed_blocks && fr.total_blocks == fg.total_blocks);
+            const SparseAttentionOutput so = block_sparse_attention(in, ref, grid);
+            const SparseAttentionOutput sg = b200::block_sparse_attention(in, got, grid);
+            double mean = 0.0;
+            CHECK(max_abs_diff(so.output, sg.output, &mean) < 2e-2);
+            CHECK(mean < 1e-3);
+            CHECK(so.coverage == sg.coverage);
+        }
+        double mean = 0.0;
+        CHECK(max_abs_diff(full_attention(in), b200::full_attention(in), &mean) < 2e-2 && mean < 1e-3);
+    }
+    // error classes (test_selection.cpp:390-405, test_sparse_exec.cpp:116-131)
+    {
+        const HeadInput in = sink_head(95, 128, 8);
+        const BlockGrid grid(128, 64, 32);
+        const QuantizedMatrix q4 = quantize_per_token(in.query);
+        const QuantizedMatrix k4 = quantize_per_key_block(in.key, grid);
+        SelectionConfig cfg;
+        CHECK_THROWS_AS(b200::selection_pass(in, q4, q4, cfg), std::invalid_argument);
+        cfg.tau = 1.0;
+        CHECK_THROWS_AS(b200::selection_pass(in, q4, k4, cfg), std::invalid_argument);
+        BlockMask none(2, 4);
+        CHECK_THROWS_AS(b200::block_sparse_attention(in, none, grid), std::domain_error);
+        const BlockGrid other(256, 64, 32);
+        BlockMask all(4, 8);
+        all.set_all(true);
+        CHECK_THROWS_AS(b200::block_sparse_attention(in, all, grid), std::invalid_argument);
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL OK", failures);
+    return failures ? 1 : 0;
+}
