@@ -9,20 +9,21 @@
 // x one 128-row query tile x a chunk of up to kSegPerUnit middle segments.
 //   * The 128-row tile pairs query blocks (2m+1, 2m+2): both have the same
 //     full-segment count F = m-1, so one key range
-//     serves both.
-//   * A (the 4 heads' Q codes, 4 x 128 rows x 128 int8) is written ONCE into
-//     TMEM (tcgen05.st, 32 columns per head) and read by every MMA from there:
-//     only K codes stream from shared memory. With A in SMEM an M=128 i8 MMA
-//     reads (M+N)*K bytes per M*N*K MACs, which at small N exceeds the 128 B/clk
-//     shared-memory port; with A in TMEM it is N*K bytes.
-//   * Keys stream through a 16-deep TMA ring of 32-key stages (one key block,
-//     4 KB); one stage feeds all 4 heads (4 x 4 MMAs of M=128, N=32, K=32)
-//     into one of three 128-column accumulator buffers.
+//     serves both. A = 4 heads x [128 rows x 128 int8 codes] (64 KB) is loaded
+//     once by TMA.
+//   * One stage = one segment = 128 keys (16 KB) through a 6-deep TMA ring.
+//     Every tcgen05.mma has N = 128 (profiles/r1_mma_microbench.txt: an MMA
+//     instruction costs >= 46 cycles whatever its N, so N = 32/64 tiles waste
+//     the tensor core; at N >= 128 i8 runs at 8192 MAC/clk/SM).
+//   * TMEM holds two 256-column accumulator buffers; each stage is issued as two
+//     groups of two heads (2 heads x 4 K-steps of M=128, N=128, K=32), group g
+//     into buffer g, so the epilogue drains one group while the other computes
+//     and each K-code stage is still shared by 4 heads (M = 512 rows per byte).
 //   * Epilogue (16 warps = 4 lane quadrants x 4 heads, thread = row):
-//     tcgen05.ld .pack::16b (|products| <= 128*49 fits int16), 16-bit SIMD max,
-//     est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max, est >= fb_row —
-//     the reference's float arithmetic. Rows OR per segment (4 stages) with a
-//     warp vote; segments are OR-ed into the packed mask with atomicOr.
+//     tcgen05.ld .pack::16b (|products| <= 128*49 fits int16), 16-bit SIMD max
+//     per 32-key block, est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max,
+//     est >= fb_row — the reference's float arithmetic. A warp vote ORs rows,
+//     atomicOr ORs segments into the packed mask.
 #include "common.cuh"
 #include "internal.h"
 
@@ -31,23 +32,23 @@ namespace sale_b200 {
 constexpr int kSegPerUnit = 64;            // segments per work unit (8192 keys)
 constexpr int kSegWords = kSegPerUnit / 32;
 constexpr int kEstHeads = 4;               // query heads per CTA
-constexpr int kEstStages = 16;             // TMA ring depth
-constexpr int kStageKeys = kBlockK;        // keys per stage (one key block)
-constexpr int kBStageBytes = kStageKeys * kHeadDim; // 4 KB
-constexpr int kAccBufs = 3;                // accumulator buffers (128 columns each)
-constexpr uint32_t kColAcc = 128;          // TMEM: A codes [0,128) | acc [128,512)
+constexpr int kEstStages = 6;              // TMA ring depth
+constexpr int kStageKeys = kSegment * kBlockK;       // 128 keys = one segment
+constexpr int kATileBytes = 128 * kHeadDim;          // 16 KB per head
+constexpr int kBStageBytes = kStageKeys * kHeadDim;  // 16 KB
 constexpr int kEpiWarps = 16;              // one (lane quadrant, query head) per warp
 constexpr int kEstThreads = 128 + 32 * kEpiWarps; // warps 0-3 control, 4-19 epilogue
 
 static_assert(kSegPerUnit == kSegPerUnitHost, "unit size mismatch");
 
 struct EstSmem {
+    alignas(1024) uint8_t a[kEstHeads][kATileBytes];
     alignas(1024) uint8_t bst[kEstStages][kBStageBytes];
     uint64_t full[kEstStages];
     uint64_t empty[kEstStages];
-    uint64_t a_ready;
-    uint64_t tmem_full[kAccBufs];
-    uint64_t tmem_empty[kAccBufs];
+    uint64_t a_full;
+    uint64_t tmem_full[2];
+    uint64_t tmem_empty[2];
     uint32_t tmem_base;
     uint32_t seg_bits[kEstHeads][2][kSegWords];
 };
@@ -55,7 +56,7 @@ struct EstSmem {
 namespace {
 
 __global__ void __launch_bounds__(kEstThreads, 1)
-estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restrict__ q_codes,
+estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_kc,
                 const EstUnit *__restrict__ units, const float *__restrict__ q_scales,
                 const float *__restrict__ k_scales, const float *__restrict__ thresh,
                 uint32_t *__restrict__ mask, int64_t tokens, int hq, int hkv, int nsub,
@@ -75,22 +76,23 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
     const int group = hq / hkv;
     const int h0 = g * group + sub * kEstHeads;
     const int nh = min(kEstHeads, group - sub * kEstHeads);
+    const int ngroups = (nh + 1) / 2;          // MMA groups of 2 heads
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t words = (nk + 31) / 32;
-    const int nstages = kSegment * u.nseg;
+    const int nstages = u.nseg;
     const int row0 = 128 * u.m + 64;
-    const int key_base = kBlockK + kSegment * kBlockK * kSegPerUnit * u.c; // first key of the unit
+    const int key_base = kBlockK + kStageKeys * kSegPerUnit * u.c; // first key of the unit
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kEstStages; ++s) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], 1);
         }
-        mbar_init(&sm.a_ready, kEpiWarps);
-        for (int s = 0; s < kAccBufs; ++s) {
+        mbar_init(&sm.a_full, 1);
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.tmem_full[s], 1);
-            mbar_init(&sm.tmem_empty[s], kEpiWarps);
+            mbar_init(&sm.tmem_empty[s], 8); // the 8 epilogue warps of the group's 2 heads
         }
         for (int hh = 0; hh < kEstHeads; ++hh)
             for (int x = 0; x < 2; ++x)
@@ -106,7 +108,11 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
     if (warp == 0) {
         // ---------------------------------------------------------- TMA producer
         if (elect_one()) {
+            tma_prefetch(&tm_qc);
             tma_prefetch(&tm_kc);
+            mbar_expect_tx(&sm.a_full, static_cast<uint32_t>(nh * kATileBytes));
+            for (int hh = 0; hh < nh; ++hh)
+                tma_load_4d(sm.a[hh], &tm_qc, &sm.a_full, 0, h0 + hh, row0, b);
             for (int k = 0; k < nstages; ++k) {
                 const int st = k % kEstStages;
                 mbar_wait(&sm.empty[st], ((k / kEstStages) & 1) ^ 1);
@@ -118,23 +124,29 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
         // ------------------------------------------------------------ MMA issuer
         if (elect_one()) {
             constexpr uint32_t idesc = idesc_i8(128, kStageKeys);
-            mbar_wait(&sm.a_ready, 0);
+            uint64_t adesc[kEstHeads];
+            for (int hh = 0; hh < kEstHeads; ++hh)
+                adesc[hh] = umma_desc_sw128(smem_u32(sm.a[hh]), 16, 1024);
+            mbar_wait(&sm.a_full, 0);
             tc_fence_after();
             for (int k = 0; k < nstages; ++k) {
                 const int st = k % kEstStages;
-                const int bb = k % kAccBufs;
                 mbar_wait(&sm.full[st], (k / kEstStages) & 1);
-                mbar_wait(&sm.tmem_empty[bb], ((k / kAccBufs) & 1) ^ 1);
-                tc_fence_after();
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.bst[st]), 16, 1024);
-                for (int hh = 0; hh < nh; ++hh) {
-                    const uint32_t d = tmem + kColAcc + bb * 128 + hh * kStageKeys;
+                for (int grp = 0; grp < ngroups; ++grp) {
+                    mbar_wait(&sm.tmem_empty[grp], (k & 1) ^ 1);
+                    tc_fence_after();
+                    for (int x = 0; x < 2; ++x) {
+                        const int hh = 2 * grp + x;
+                        if (hh >= nh) break;
+                        const uint32_t d = tmem + 256 * grp + 128 * x;
 #pragma unroll
-                    for (int kk = 0; kk < kHeadDim / 32; ++kk) // K = 32 int8 = 8 TMEM columns
-                        mma_i8_ts(d, tmem + hh * 32 + 8 * kk, bdesc + 2 * kk, idesc, kk > 0);
+                        for (int kk = 0; kk < kHeadDim / 32; ++kk)
+                            mma_i8_ss(d, adesc[hh] + 2 * kk, bdesc + 2 * kk, idesc, kk > 0);
+                    }
+                    tc_commit(&sm.tmem_full[grp]);
                 }
                 tc_commit(&sm.empty[st]);
-                tc_commit(&sm.tmem_full[bb]);
             }
         }
     } else if (warp >= 4) {
@@ -145,69 +157,56 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
         const int64_t tok = row0 + r;
         const bool row_ok = tok < tokens;
         const int hh = ew >> 2;               // this warp's query head (0..3)
+        const int grp = hh >> 1;
         const bool active = hh < nh;          // warp-uniform
-        const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 256 * grp +
+                             128 * (hh & 1);
         float qs = 0.0f, fb = INFINITY;
-        bool flag = false;
-        // A operand: this row's 128 codes -> TMEM columns [32 hh, 32 hh + 32)
-        if (active) {
-            uint32_t a[32];
-            if (row_ok) {
-                const uint4 *src = reinterpret_cast<const uint4 *>(
-                    q_codes + ((static_cast<int64_t>(b) * tokens + tok) * hq + h0 + hh) * kHeadDim);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint4 w = __ldg(src + e);
-                    a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
-                }
-                const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
-                qs = q_scales[o];
-                fb = thresh[o];
-            } else {
-#pragma unroll
-                for (int e = 0; e < 32; ++e) a[e] = 0u;
-            }
-            tmem_st32(lane_addr + hh * 32, a);
-            tmem_st_wait();
+        if (active && row_ok) {
+            const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
+            qs = q_scales[o];
+            fb = thresh[o];
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.a_ready);
-
         const float *ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
         const int64_t jb_base = key_base / kBlockK;
-        for (int k = 0; k < nstages; ++k) {
-            const int bb = k % kAccBufs;
-            const float ks = ks_row[jb_base + k];
-            mbar_wait(&sm.tmem_full[bb], (k / kAccBufs) & 1);
-            tc_fence_after();
-            if (active) {
-                uint32_t v[16];
-                tmem_ld32_pack16(lane_addr + kColAcc + bb * 128 + hh * kStageKeys, v);
-                tmem_ld_wait();
+        if (grp < ngroups) {
+            for (int k = 0; k < nstages; ++k) {
+                const float *ksp = ks_row + jb_base + 4 * k; // 4 key blocks of segment k
+                const float4 ks = make_float4(ksp[0], ksp[1], ksp[2], ksp[3]);
+                mbar_wait(&sm.tmem_full[grp], k & 1);
+                tc_fence_after();
+                bool flag = false;
+                if (active) {
+                    uint32_t v[4][16];
 #pragma unroll
-                for (int s = 8; s > 0; s >>= 1)
+                    for (int jb = 0; jb < 4; ++jb) tmem_ld32_pack16(acc + 32 * jb, v[jb]);
+                    tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < s; ++e) v[e] = __vmaxs2(v[e], v[e + s]);
-                const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
-                const int hi = static_cast<int16_t>(v[0] >> 16);
-                const int mx = lo > hi ? lo : hi;
-                const float rs = __fmul_rn(__fmul_rn(qs, ks), inv_sqrt_d);
-                const float est = __fmul_rn(rs, static_cast<float>(mx));
-                flag |= est >= fb;
-                if (dbg_max != nullptr && row_ok)
-                    dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                            jb_base + k] = mx;
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.tmem_empty[bb]);
-            if ((k & 3) == 3 && active) {
-                const int seg = k >> 2;
-                const bool any = __any_sync(0xffffffffu, flag);
-                if (lane == 0 && any)
-                    atomicOr(&sm.seg_bits[hh][quad >> 1][seg >> 5], 1u << (seg & 31));
-                flag = false;
+                    for (int jb = 0; jb < 4; ++jb) {
+#pragma unroll
+                        for (int s = 8; s > 0; s >>= 1)
+#pragma unroll
+                            for (int e = 0; e < s; ++e) v[jb][e] = __vmaxs2(v[jb][e], v[jb][e + s]);
+                        const int lo = static_cast<int16_t>(v[jb][0] & 0xFFFFu);
+                        const int hi = static_cast<int16_t>(v[jb][0] >> 16);
+                        const int mx = lo > hi ? lo : hi;
+                        const float ksj = jb == 0 ? ks.x : jb == 1 ? ks.y : jb == 2 ? ks.z : ks.w;
+                        const float rs = __fmul_rn(__fmul_rn(qs, ksj), inv_sqrt_d);
+                        const float est = __fmul_rn(rs, static_cast<float>(mx));
+                        flag |= est >= fb;
+                        if (dbg_max != nullptr && row_ok)
+                            dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                                    jb_base + 4 * k + jb] = mx;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.tmem_empty[grp]);
+                if (active) {
+                    const bool any = __any_sync(0xffffffffu, flag);
+                    if (lane == 0 && any)
+                        atomicOr(&sm.seg_bits[hh][quad >> 1][k >> 5], 1u << (k & 31));
+                }
             }
         }
         named_bar_sync(1, 32 * kEpiWarps);
@@ -243,7 +242,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
 
 size_t estimate_smem_bytes() { return sizeof(EstSmem) + 1024; }
 
-cudaError_t launch_estimate(const CUtensorMap &tm_kc, const int8_t *q_codes, const EstUnit *units,
+cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
                             int64_t n_units, const float *q_scales, const float *k_scales,
                             const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
                             int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
@@ -261,7 +260,7 @@ cudaError_t launch_estimate(const CUtensorMap &tm_kc, const int8_t *q_codes, con
     const int group = hq / hkv;
     const int nsub = (group + kEstHeads - 1) / kEstHeads;
     dim3 grid(static_cast<unsigned>(n_units), static_cast<unsigned>(batch * hkv * nsub));
-    estimate_kernel<<<grid, kEstThreads, smem, stream>>>(tm_kc, q_codes, units, q_scales, k_scales,
+    estimate_kernel<<<grid, kEstThreads, smem, stream>>>(tm_qc, tm_kc, units, q_scales, k_scales,
                                                          thresh, mask, tokens, hq, hkv, nsub,
                                                          inv_sqrt_d, dbg_max);
     return cudaGetLastError();
