@@ -99,6 +99,21 @@ template <int NK>
 __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uint32_t nib,
                                              int64_t lim, float scale_log2, SoftmaxState &st,
                                              uint64_t *pv_prev, uint32_t pv_parity) {
+    // The other head of the pair selected this tile, this warp's rows did not
+    // (or they are all in the causal future): P = 0, no exp work.
+    if (__all_sync(0xffffffffu, nib == 0u || lim < 0)) {
+        uint32_t z[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) z[e] = 0u;
+        if constexpr (NK == 128) {
+            tmem_st32(sAddr, z);
+            tmem_st32(sAddr + 32, z);
+        } else {
+            tmem_st16(sAddr, *reinterpret_cast<uint32_t(*)[16]>(&z[0]));
+        }
+        tmem_st_wait();
+        return;
+    }
     uint32_t s[NK];
 #pragma unroll
     for (int c4 = 0; c4 < NK / 32; ++c4)

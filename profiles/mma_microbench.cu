@@ -78,7 +78,70 @@ template <int KIND, int N, bool A_TMEM> void run(const char *name) {
     cudaFree(d);
 }
 
+// Distinct A (16 KB) and B (16 KB) regions: SMEM must deliver both operands.
+template <int KIND>
+__global__ void __launch_bounds__(128, 1) mma_bench_distinct(int iters, unsigned long long *cycles) {
+    __shared__ __align__(1024) uint8_t a[128 * 128];
+    __shared__ __align__(1024) uint8_t bsm[128 * 128];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    for (int i = threadIdx.x; i < 128 * 128 / 4; i += 128) {
+        reinterpret_cast<uint32_t *>(a)[i] = 0x01010101u * (i & 3);
+        reinterpret_cast<uint32_t *>(bsm)[i] = 0x01010101u * (i & 5);
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    if (threadIdx.x < 32) tmem_alloc<512>(&tbase);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tbase;
+    if (threadIdx.x == 0) {
+        const uint32_t idesc = KIND == 0 ? idesc_i8(128, 128) : idesc_bf16(128, 128, false);
+        const uint64_t ad = umma_desc_sw128(smem_u32(a), 16, 1024);
+        const uint64_t bd = umma_desc_sw128(smem_u32(bsm), 16, 1024);
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            const uint32_t d = tmem + 128 * (it & 3);
+            if (KIND == 0) mma_i8_ss(d, ad + 2 * (it & 3), bd + 2 * (it & 3), idesc, it > 3);
+            else mma_bf16_ss(d, ad + 2 * (it & 3), bd + 2 * (it & 3), idesc, it > 3);
+        }
+        tc_commit(&bar);
+        mbar_wait(&bar, 0);
+        const long long t1 = clock64();
+        atomicAdd(cycles, static_cast<unsigned long long>(t1 - t0));
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int KIND> void run_distinct(const char *name) {
+    unsigned long long *d;
+    cudaMalloc(&d, 8);
+    const int iters = 4096, ctas = 148;
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaMemset(d, 0, 8);
+        mma_bench_distinct<KIND><<<ctas, 128>>>(iters, d);
+        cudaDeviceSynchronize();
+    }
+    unsigned long long c;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    const double cyc = static_cast<double>(c) / ctas / iters;
+    const double macs = 128.0 * 128 * 32.0 / (KIND == 0 ? 1 : 2);
+    printf("%-28s %7.1f cycles/MMA  %8.0f MAC/clk/SM\n", name, cyc, macs / cyc);
+    cudaFree(d);
+}
+
 int main() {
+    run_distinct<0>("i8  M128 N128 SS distinct");
+    run_distinct<1>("bf16 M128 N128 SS distinct");
     run<0, 32, true>("i8  M128 N32  A=TMEM");
     run<0, 64, true>("i8  M128 N64  A=TMEM");
     run<0, 128, true>("i8  M128 N128 A=TMEM");
