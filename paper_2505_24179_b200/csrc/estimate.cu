@@ -92,7 +92,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         mbar_init(&sm.a_full, 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.tmem_full[s], 1);
-            mbar_init(&sm.tmem_empty[s], 8); // the 8 epilogue warps of the group's 2 heads
+            mbar_init(&sm.tmem_empty[s], kEpiWarps); // all epilogue warps drain every group
         }
         for (int hh = 0; hh < kEstHeads; ++hh)
             for (int x = 0; x < 2; ++x)
@@ -156,33 +156,40 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const int r = quad * 32 + lane;       // row within the 128-row tile
         const int64_t tok = row0 + r;
         const bool row_ok = tok < tokens;
-        const int hh = ew >> 2;               // this warp's query head (0..3)
-        const int grp = hh >> 1;
-        const bool active = hh < nh;          // warp-uniform
-        const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 256 * grp +
-                             128 * (hh & 1);
-        float qs = 0.0f, fb = INFINITY;
-        if (active && row_ok) {
-            const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
-            qs = q_scales[o];
-            fb = thresh[o];
+        // Every group is drained by all 16 warps: warp = (quadrant, head of the
+        // group's pair, column half = key blocks {2c, 2c+1} of the segment).
+        const int hx = (ew >> 2) & 1;
+        const int ch = ew >> 3;
+        float qs[2] = {0.0f, 0.0f}, fb[2] = {INFINITY, INFINITY};
+#pragma unroll
+        for (int grp = 0; grp < 2; ++grp) {
+            const int hh = 2 * grp + hx;
+            if (hh < nh && row_ok) {
+                const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
+                qs[grp] = q_scales[o];
+                fb[grp] = thresh[o];
+            }
         }
         const float *ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
         const int64_t jb_base = key_base / kBlockK;
-        if (grp < ngroups) {
-            for (int k = 0; k < nstages; ++k) {
-                const float *ksp = ks_row + jb_base + 4 * k; // 4 key blocks of segment k
-                const float4 ks = make_float4(ksp[0], ksp[1], ksp[2], ksp[3]);
+        for (int k = 0; k < nstages; ++k) {
+            const float *ksp = ks_row + jb_base + 4 * k + 2 * ch; // this warp's 2 key blocks
+            const float ks0 = ksp[0], ks1 = ksp[1];
+            for (int grp = 0; grp < ngroups; ++grp) {
+                const int hh = 2 * grp + hx;
+                const bool active = hh < nh; // warp-uniform
                 mbar_wait(&sm.tmem_full[grp], k & 1);
                 tc_fence_after();
                 bool flag = false;
                 if (active) {
-                    uint32_t v[4][16];
-#pragma unroll
-                    for (int jb = 0; jb < 4; ++jb) tmem_ld32_pack16(acc + 32 * jb, v[jb]);
+                    const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) +
+                                         256 * grp + 128 * hx + 64 * ch;
+                    uint32_t v[2][16];
+                    tmem_ld32_pack16(acc, v[0]);
+                    tmem_ld32_pack16(acc + 32, v[1]);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int jb = 0; jb < 4; ++jb) {
+                    for (int jb = 0; jb < 2; ++jb) {
 #pragma unroll
                         for (int s = 8; s > 0; s >>= 1)
 #pragma unroll
@@ -190,13 +197,12 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                         const int lo = static_cast<int16_t>(v[jb][0] & 0xFFFFu);
                         const int hi = static_cast<int16_t>(v[jb][0] >> 16);
                         const int mx = lo > hi ? lo : hi;
-                        const float ksj = jb == 0 ? ks.x : jb == 1 ? ks.y : jb == 2 ? ks.z : ks.w;
-                        const float rs = __fmul_rn(__fmul_rn(qs, ksj), inv_sqrt_d);
+                        const float rs = __fmul_rn(__fmul_rn(qs[grp], jb ? ks1 : ks0), inv_sqrt_d);
                         const float est = __fmul_rn(rs, static_cast<float>(mx));
-                        flag |= est >= fb;
+                        flag |= est >= fb[grp];
                         if (dbg_max != nullptr && row_ok)
                             dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                                    jb_base + 4 * k + jb] = mx;
+                                    jb_base + 4 * k + 2 * ch + jb] = mx;
                     }
                 }
                 tc_fence_before();
