@@ -163,14 +163,50 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
     const float neg_m = st.m_run == -INFINITY ? 0.0f : -st.m_run;
     const unsigned long long sc2 = pack_f2(scale_log2, scale_log2), nm2 = pack_f2(neg_m, neg_m);
     unsigned long long psum2 = 0ull;
+    if (NK == 128 && __all_sync(0xffffffffu, full)) {
+        // Full tiles: one pair in four takes exp2 on the FMA pipe (Cody-Waite
+        // split + degree-3 polynomial, rel. err 1e-4 < bf16's 2^-8) so the
+        // MUFU pipe (16 ex2/clk/SM) stops being the co-bottleneck with the MMA.
 #pragma unroll
-    for (int c2 = 0; c2 < NK / 2; ++c2) {
-        unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
-        ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
-        const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
-        const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
-        fadd2_f32(psum2, pack_f2(p0, p1));
-        s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
+        for (int c2 = 0; c2 < NK / 2; ++c2) {
+            unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
+            ffma2_f32(x, sc2, nm2);
+            float p0, p1;
+            if ((c2 & 3) == 3) {
+                const unsigned long long xc =
+                    pack_f2(fmaxf(__uint_as_float(static_cast<uint32_t>(x)), -125.0f),
+                            fmaxf(__uint_as_float(static_cast<uint32_t>(x >> 32)), -125.0f));
+                unsigned long long t = xc;
+                fadd2_f32(t, pack_f2(12582912.0f, 12582912.0f));   // round to integer
+                unsigned long long r = t;
+                fadd2_f32(r, pack_f2(-12582912.0f, -12582912.0f)); // the integer, as float
+                unsigned long long f = r ^ 0x8000000080000000ull;  // -r
+                fadd2_f32(f, xc);                                  // f = x - r in [-.5, .5]
+                unsigned long long pp = pack_f2(0.05592204f, 0.05592204f);
+                ffma2_f32(pp, f, pack_f2(0.24264008f, 0.24264008f));
+                ffma2_f32(pp, f, pack_f2(0.69312102f, 0.69312102f));
+                ffma2_f32(pp, f, pack_f2(0.99992448f, 0.99992448f));
+                p0 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp)) +
+                                    (static_cast<int>(static_cast<uint32_t>(t)) << 23));
+                p1 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp >> 32)) +
+                                    (static_cast<int>(static_cast<uint32_t>(t >> 32)) << 23));
+            } else {
+                p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
+                p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
+            }
+            fadd2_f32(psum2, pack_f2(p0, p1));
+            s[c2] = pack_bf16x2(p0, p1);
+        }
+    } else {
+#pragma unroll
+        for (int c2 = 0; c2 < NK / 2; ++c2) {
+            unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
+            ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
+            const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
+            const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
+            fadd2_f32(psum2, pack_f2(p0, p1));
+            s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
+        }
     }
     st.l_run += __uint_as_float(static_cast<uint32_t>(psum2)) +
                 __uint_as_float(static_cast<uint32_t>(psum2 >> 32));
