@@ -15,11 +15,11 @@
 //     Every tcgen05.mma has N = 128 (profiles/r1_mma_microbench.txt: an MMA
 //     instruction costs >= 46 cycles whatever its N, so N = 32/64 tiles waste
 //     the tensor core; at N >= 128 i8 runs at 8192 MAC/clk/SM).
-//   * TMEM holds two 256-column accumulator buffers; each stage is issued as two
-//     groups of two heads (2 heads x 4 K-steps of M=128, N=128, K=32), group g
-//     into buffer g, so the epilogue drains one group while the other computes
-//     and each K-code stage is still shared by 4 heads (M = 512 rows per byte).
-//   * Epilogue (16 warps = 4 lane quadrants x 4 heads, thread = row):
+//   * TMEM holds one 128-column accumulator per head; a stage is 4 heads x 4
+//     K-steps of M=128, N=128, K=32, head h into buffer h, so head h's epilogue
+//     has the other three heads' MMAs to drain its buffer, and each K-code
+//     stage is shared by 4 heads (M = 512 rows per byte of K).
+//   * Epilogue (16 warps = 4 lane quadrants x 4 key blocks, thread = row):
 //     tcgen05.ld .pack::16b (|products| <= 128*49 fits int16), 16-bit SIMD max
 //     per 32-key block, est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max,
 //     est >= fb_row — the reference's float arithmetic. A warp vote ORs rows,
@@ -47,8 +47,8 @@ struct EstSmem {
     uint64_t full[kEstStages];
     uint64_t empty[kEstStages];
     uint64_t a_full;
-    uint64_t tmem_full[2];
-    uint64_t tmem_empty[2];
+    uint64_t tmem_full[kEstHeads];
+    uint64_t tmem_empty[kEstHeads];
     uint32_t tmem_base;
     uint32_t seg_bits[kEstHeads][2][kSegWords];
 };
@@ -76,7 +76,6 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
     const int group = hq / hkv;
     const int h0 = g * group + sub * kEstHeads;
     const int nh = min(kEstHeads, group - sub * kEstHeads);
-    const int ngroups = (nh + 1) / 2;          // MMA groups of 2 heads
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t words = (nk + 31) / 32;
@@ -90,7 +89,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             mbar_init(&sm.empty[s], 1);
         }
         mbar_init(&sm.a_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kEstHeads; ++s) {
             mbar_init(&sm.tmem_full[s], 1);
             mbar_init(&sm.tmem_empty[s], kEpiWarps); // all epilogue warps drain every group
         }
@@ -133,18 +132,16 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 const int st = k % kEstStages;
                 mbar_wait(&sm.full[st], (k / kEstStages) & 1);
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.bst[st]), 16, 1024);
-                for (int grp = 0; grp < ngroups; ++grp) {
-                    mbar_wait(&sm.tmem_empty[grp], (k & 1) ^ 1);
+                for (int hh = 0; hh < nh; ++hh) {
+                    // head hh owns TMEM columns [128 hh, 128 hh + 128): its
+                    // epilogue of stage k-1 had three other heads' MMAs to finish
+                    mbar_wait(&sm.tmem_empty[hh], (k & 1) ^ 1);
                     tc_fence_after();
-                    for (int x = 0; x < 2; ++x) {
-                        const int hh = 2 * grp + x;
-                        if (hh >= nh) break;
-                        const uint32_t d = tmem + 256 * grp + 128 * x;
+                    const uint32_t d = tmem + 128 * hh;
 #pragma unroll
-                        for (int kk = 0; kk < kHeadDim / 32; ++kk)
-                            mma_i8_ss(d, adesc[hh] + 2 * kk, bdesc + 2 * kk, idesc, kk > 0);
-                    }
-                    tc_commit(&sm.tmem_full[grp]);
+                    for (int kk = 0; kk < kHeadDim / 32; ++kk)
+                        mma_i8_ss(d, adesc[hh] + 2 * kk, bdesc + 2 * kk, idesc, kk > 0);
+                    tc_commit(&sm.tmem_full[hh]);
                 }
                 tc_commit(&sm.empty[st]);
             }
@@ -156,63 +153,50 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const int r = quad * 32 + lane;       // row within the 128-row tile
         const int64_t tok = row0 + r;
         const bool row_ok = tok < tokens;
-        // Every group is drained by all 16 warps: warp = (quadrant, head of the
-        // group's pair, column half = key blocks {2c, 2c+1} of the segment).
-        const int hx = (ew >> 2) & 1;
-        const int ch = ew >> 3;
-        float qs[2] = {0.0f, 0.0f}, fb[2] = {INFINITY, INFINITY};
+        // Every head's buffer is drained by all 16 warps: warp = (quadrant,
+        // key block `chunk` of the segment = 32 accumulator columns).
+        const int chunk = ew >> 2;
+        float qs[kEstHeads], fb[kEstHeads];
 #pragma unroll
-        for (int grp = 0; grp < 2; ++grp) {
-            const int hh = 2 * grp + hx;
+        for (int hh = 0; hh < kEstHeads; ++hh) {
+            qs[hh] = 0.0f;
+            fb[hh] = INFINITY;
             if (hh < nh && row_ok) {
                 const int64_t o = (static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok;
-                qs[grp] = q_scales[o];
-                fb[grp] = thresh[o];
+                qs[hh] = q_scales[o];
+                fb[hh] = thresh[o];
             }
         }
         const float *ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
         const int64_t jb_base = key_base / kBlockK;
+        const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 32 * chunk;
         for (int k = 0; k < nstages; ++k) {
-            const float *ksp = ks_row + jb_base + 4 * k + 2 * ch; // this warp's 2 key blocks
-            const float ks0 = ksp[0], ks1 = ksp[1];
-            for (int grp = 0; grp < ngroups; ++grp) {
-                const int hh = 2 * grp + hx;
-                const bool active = hh < nh; // warp-uniform
-                mbar_wait(&sm.tmem_full[grp], k & 1);
+            const float ks = ks_row[jb_base + 4 * k + chunk];
+#pragma unroll
+            for (int hh = 0; hh < kEstHeads; ++hh) {
+                if (hh >= nh) break; // warp-uniform
+                mbar_wait(&sm.tmem_full[hh], k & 1);
                 tc_fence_after();
-                bool flag = false;
-                if (active) {
-                    const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) +
-                                         256 * grp + 128 * hx + 64 * ch;
-                    uint32_t v[2][16];
-                    tmem_ld32_pack16(acc, v[0]);
-                    tmem_ld32_pack16(acc + 32, v[1]);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int jb = 0; jb < 2; ++jb) {
-#pragma unroll
-                        for (int s = 8; s > 0; s >>= 1)
-#pragma unroll
-                            for (int e = 0; e < s; ++e) v[jb][e] = __vmaxs2(v[jb][e], v[jb][e + s]);
-                        const int lo = static_cast<int16_t>(v[jb][0] & 0xFFFFu);
-                        const int hi = static_cast<int16_t>(v[jb][0] >> 16);
-                        const int mx = lo > hi ? lo : hi;
-                        const float rs = __fmul_rn(__fmul_rn(qs[grp], jb ? ks1 : ks0), inv_sqrt_d);
-                        const float est = __fmul_rn(rs, static_cast<float>(mx));
-                        flag |= est >= fb[grp];
-                        if (dbg_max != nullptr && row_ok)
-                            dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                                    jb_base + 4 * k + 2 * ch + jb] = mx;
-                    }
-                }
+                uint32_t v[16];
+                tmem_ld32_pack16(acc + 128 * hh, v);
+                tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.tmem_empty[grp]);
-                if (active) {
-                    const bool any = __any_sync(0xffffffffu, flag);
-                    if (lane == 0 && any)
-                        atomicOr(&sm.seg_bits[hh][quad >> 1][k >> 5], 1u << (k & 31));
-                }
+                if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]); // registers hold the data now
+#pragma unroll
+                for (int s = 8; s > 0; s >>= 1)
+#pragma unroll
+                    for (int e = 0; e < s; ++e) v[e] = __vmaxs2(v[e], v[e + s]);
+                const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
+                const int hi = static_cast<int16_t>(v[0] >> 16);
+                const int mx = lo > hi ? lo : hi;
+                const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
+                const float est = __fmul_rn(rs, static_cast<float>(mx));
+                if (dbg_max != nullptr && row_ok)
+                    dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                            jb_base + 4 * k + chunk] = mx;
+                const bool any = __any_sync(0xffffffffu, est >= fb[hh]);
+                if (lane == 0 && any) atomicOr(&sm.seg_bits[hh][quad >> 1][k >> 5], 1u << (k & 31));
             }
         }
         named_bar_sync(1, 32 * kEpiWarps);
