@@ -155,6 +155,11 @@ int sale_b200_synchronize(sale_b200_ctx *ctx);
  * between kernels; sale_b200_stage_times waits for the last one and returns
  * ms[5] = quantize, base mask, sink-local stats, estimator, attention. */
 int sale_b200_set_timing(sale_b200_ctx *ctx, int enable);
+/* Estimator wait-time counters (cycles, summed over CTAs): counters[8] =
+ * MMA-issuer loop, A wait, K-stage waits, accumulator waits, stages,
+ * epilogue loop (warp 4), epilogue accumulator waits, 0. Reads and resets;
+ * enable != 0 turns collection on for later launches. counters may be NULL. */
+int sale_b200_estimator_profile(sale_b200_ctx *ctx, int enable, uint64_t *counters);
 int sale_b200_stage_times(sale_b200_ctx *ctx, float *ms);
 
 /* ---- synthetic workload (host, not the hot path) --------------------------

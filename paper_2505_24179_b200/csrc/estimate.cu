@@ -53,6 +53,12 @@ struct EstSmem {
     uint32_t seg_bits[kEstHeads][2][kSegWords];
 };
 
+// Optional wait-time instrumentation (sale_b200_est_profile): cycles the MMA
+// issuer spends blocked on K stages / accumulator buffers, and the epilogue on
+// accumulators. Off unless enabled; one global flag read per CTA.
+__device__ int g_est_prof_on = 0;
+__device__ unsigned long long g_est_prof[8];
+
 namespace {
 
 __global__ void __launch_bounds__(kEstThreads, 1)
@@ -126,16 +132,23 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             uint64_t adesc[kEstHeads];
             for (int hh = 0; hh < kEstHeads; ++hh)
                 adesc[hh] = umma_desc_sw128(smem_u32(sm.a[hh]), 16, 1024);
+            const bool prof = g_est_prof_on != 0;
+            long long t_start = clock64(), w_full = 0, w_empty = 0;
             mbar_wait(&sm.a_full, 0);
+            const long long w_a = clock64() - t_start;
             tc_fence_after();
             for (int k = 0; k < nstages; ++k) {
                 const int st = k % kEstStages;
+                long long t0 = prof ? clock64() : 0;
                 mbar_wait(&sm.full[st], (k / kEstStages) & 1);
+                if (prof) w_full += clock64() - t0;
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.bst[st]), 16, 1024);
                 for (int hh = 0; hh < nh; ++hh) {
                     // head hh owns TMEM columns [128 hh, 128 hh + 128): its
                     // epilogue of stage k-1 had three other heads' MMAs to finish
+                    t0 = prof ? clock64() : 0;
                     mbar_wait(&sm.tmem_empty[hh], (k & 1) ^ 1);
+                    if (prof) w_empty += clock64() - t0;
                     tc_fence_after();
                     const uint32_t d = tmem + 128 * hh;
 #pragma unroll
@@ -144,6 +157,13 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                     tc_commit(&sm.tmem_full[hh]);
                 }
                 tc_commit(&sm.empty[st]);
+            }
+            if (prof) {
+                atomicAdd(&g_est_prof[0], static_cast<unsigned long long>(clock64() - t_start));
+                atomicAdd(&g_est_prof[1], static_cast<unsigned long long>(w_a));
+                atomicAdd(&g_est_prof[2], static_cast<unsigned long long>(w_full));
+                atomicAdd(&g_est_prof[3], static_cast<unsigned long long>(w_empty));
+                atomicAdd(&g_est_prof[4], static_cast<unsigned long long>(nstages));
             }
         }
     } else if (warp >= 4) {
@@ -170,12 +190,17 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const float *ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
         const int64_t jb_base = key_base / kBlockK;
         const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 32 * chunk;
+        const bool prof = ew == 0 && g_est_prof_on != 0;
+        long long w_epi = 0;
+        const long long t_epi = clock64();
         for (int k = 0; k < nstages; ++k) {
             const float ks = ks_row[jb_base + 4 * k + chunk];
 #pragma unroll
             for (int hh = 0; hh < kEstHeads; ++hh) {
                 if (hh >= nh) break; // warp-uniform
+                const long long t0 = prof ? clock64() : 0;
                 mbar_wait(&sm.tmem_full[hh], k & 1);
+                if (prof) w_epi += clock64() - t0;
                 tc_fence_after();
                 uint32_t v[16];
                 tmem_ld32_pack16(acc + 128 * hh, v);
@@ -198,6 +223,10 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 const bool any = __any_sync(0xffffffffu, est >= fb[hh]);
                 if (lane == 0 && any) atomicOr(&sm.seg_bits[hh][quad >> 1][k >> 5], 1u << (k & 31));
             }
+        }
+        if (prof && lane == 0) {
+            atomicAdd(&g_est_prof[5], static_cast<unsigned long long>(clock64() - t_epi));
+            atomicAdd(&g_est_prof[6], static_cast<unsigned long long>(w_epi));
         }
         named_bar_sync(1, 32 * kEpiWarps);
         if (ew == 0 && lane < 2 * kEstHeads) {
@@ -231,6 +260,17 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
 } // namespace
 
 size_t estimate_smem_bytes() { return sizeof(EstSmem) + 1024; }
+
+cudaError_t estimate_profile(int enable, unsigned long long *out8) {
+    if (out8) {
+        cudaError_t e = cudaMemcpyFromSymbol(out8, g_est_prof, sizeof(g_est_prof));
+        if (e != cudaSuccess) return e;
+    }
+    unsigned long long zero[8] = {};
+    cudaError_t e = cudaMemcpyToSymbol(g_est_prof, zero, sizeof(zero));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(g_est_prof_on, &enable, sizeof(int));
+}
 
 cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
                             int64_t n_units, const float *q_scales, const float *k_scales,
