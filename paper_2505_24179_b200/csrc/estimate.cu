@@ -193,37 +193,70 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const bool prof = ew == 0 && g_est_prof_on != 0;
         long long w_epi = 0;
         const long long t_epi = clock64();
+        // per-row selection flags: bit k of flags[hh][k >> 5] = some column of
+        // this row's key block in segment k passed; OR-reduced over rows once
+        uint32_t flags[kEstHeads][kSegWords];
+#pragma unroll
+        for (int hh = 0; hh < kEstHeads; ++hh)
+#pragma unroll
+            for (int w = 0; w < kSegWords; ++w) flags[hh][w] = 0u;
         for (int k = 0; k < nstages; ++k) {
             const float ks = ks_row[jb_base + 4 * k + chunk];
+            const uint32_t kbit = 1u << (k & 31);
+            const int kw = k >> 5;
+            // two heads per step: one tcgen05.wait::ld, two independent reductions
 #pragma unroll
-            for (int hh = 0; hh < kEstHeads; ++hh) {
-                if (hh >= nh) break; // warp-uniform
+            for (int hp = 0; hp < kEstHeads; hp += 2) {
+                if (hp >= nh) break; // warp-uniform
+                const bool two = hp + 1 < nh;
                 const long long t0 = prof ? clock64() : 0;
-                mbar_wait(&sm.tmem_full[hh], k & 1);
+                mbar_wait(&sm.tmem_full[hp], k & 1);
+                if (two) mbar_wait(&sm.tmem_full[hp + 1], k & 1);
                 if (prof) w_epi += clock64() - t0;
                 tc_fence_after();
-                uint32_t v[16];
-                tmem_ld32_pack16(acc + 128 * hh, v);
+                uint32_t v[2][16];
+                tmem_ld32_pack16(acc + 128 * hp, v[0]);
+                if (two) tmem_ld32_pack16(acc + 128 * (hp + 1), v[1]);
                 tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]); // registers hold the data now
+                if (lane == 0) { // registers hold the data now: release the buffers
+                    mbar_arrive(&sm.tmem_empty[hp]);
+                    if (two) mbar_arrive(&sm.tmem_empty[hp + 1]);
+                }
 #pragma unroll
-                for (int s = 8; s > 0; s >>= 1)
+                for (int x = 0; x < 2; ++x) {
+                    if (x == 1 && !two) break;
+                    const int hh = hp + x;
 #pragma unroll
-                    for (int e = 0; e < s; ++e) v[e] = __vmaxs2(v[e], v[e + s]);
-                const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
-                const int hi = static_cast<int16_t>(v[0] >> 16);
-                const int mx = lo > hi ? lo : hi;
-                const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
-                const float est = __fmul_rn(rs, static_cast<float>(mx));
-                if (dbg_max != nullptr && row_ok)
-                    dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                            jb_base + 4 * k + chunk] = mx;
-                const bool any = __any_sync(0xffffffffu, est >= fb[hh]);
-                if (lane == 0 && any) atomicOr(&sm.seg_bits[hh][quad >> 1][k >> 5], 1u << (k & 31));
+                    for (int s = 8; s > 0; s >>= 1)
+#pragma unroll
+                        for (int e = 0; e < s; ++e) v[x][e] = __vmaxs2(v[x][e], v[x][e + s]);
+                    const int lo = static_cast<int16_t>(v[x][0] & 0xFFFFu);
+                    const int hi = static_cast<int16_t>(v[x][0] >> 16);
+                    const int mx = lo > hi ? lo : hi;
+                    const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
+                    const float est = __fmul_rn(rs, static_cast<float>(mx));
+                    if (est >= fb[hh]) {
+#pragma unroll
+                        for (int w = 0; w < kSegWords; ++w)
+                            if (w == kw) flags[hh][w] |= kbit;
+                    }
+                    if (dbg_max != nullptr && row_ok)
+                        dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                                jb_base + 4 * k + chunk] = mx;
+                }
             }
         }
+        // OR over the warp's 32 rows; the two query blocks of the tile are the
+        // lane quadrants {0,1} and {2,3}
+#pragma unroll
+        for (int hh = 0; hh < kEstHeads; ++hh)
+#pragma unroll
+            for (int w = 0; w < kSegWords; ++w) {
+                const uint32_t any = __reduce_or_sync(0xffffffffu, flags[hh][w]);
+                if (lane == 0 && any && hh < nh) atomicOr(&sm.seg_bits[hh][quad >> 1][w], any);
+            }
         if (prof && lane == 0) {
             atomicAdd(&g_est_prof[5], static_cast<unsigned long long>(clock64() - t_epi));
             atomicAdd(&g_est_prof[6], static_cast<unsigned long long>(w_epi));
