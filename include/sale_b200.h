@@ -157,8 +157,11 @@ int sale_b200_synchronize(sale_b200_ctx *ctx);
 int sale_b200_set_timing(sale_b200_ctx *ctx, int enable);
 /* Estimator wait-time counters (cycles, summed over CTAs): counters[8] =
  * MMA-issuer loop, A wait, K-stage waits, accumulator waits, stages,
- * epilogue loop (warp 4), epilogue accumulator waits, 0. Reads and resets;
- * enable != 0 turns collection on for later launches. counters may be NULL. */
+ * epilogue loop (warp 4), epilogue accumulator waits, 0; then counters[8..15]
+ * = sink-local-stats phase cycles (staging, dots, logit store, block max,
+ * running max, exp sums, combine) and the CTA count. Reads and resets;
+ * enable != 0 turns collection on for later launches. counters may be NULL
+ * (then it must hold 16 entries otherwise). */
 int sale_b200_estimator_profile(sale_b200_ctx *ctx, int enable, uint64_t *counters);
 int sale_b200_stage_times(sale_b200_ctx *ctx, float *ms);
 

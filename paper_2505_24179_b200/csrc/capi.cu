@@ -369,6 +369,8 @@ int sale_b200_estimator_profile(sale_b200_ctx *ctx, int enable, uint64_t *counte
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
     SALE_CUDA(ctx, cudaDeviceSynchronize());
     SALE_CUDA(ctx, estimate_profile(enable, reinterpret_cast<unsigned long long *>(counters)));
+    SALE_CUDA(ctx, stats_profile(enable, counters ? reinterpret_cast<unsigned long long *>(counters + 8)
+                                                  : nullptr));
     return SALE_B200_OK;
 }
 

@@ -60,6 +60,16 @@ __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
     return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
 }
 
+} // namespace
+
+// Optional phase timing (sale_b200_estimator_profile counters 8..15): cycles
+// thread 0 spends in staging, dots, logit store, block max, running max, exp
+// sums, final combine; summed over CTAs.
+__device__ int g_stats_prof_on = 0;
+__device__ unsigned long long g_stats_prof[8];
+
+namespace {
+
 // grid: (nq - 3, heads, batch) — query blocks i >= 3 (non-empty middle).
 __global__ void __launch_bounds__(kThreads, 2)
 sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__restrict__ k,
@@ -70,6 +80,11 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     extern __shared__ __align__(16) uint8_t smem_raw[];
     StatsSmem &sm = *reinterpret_cast<StatsSmem *>(smem_raw);
     const int tid = threadIdx.x;
+    const bool prof = tid == 0 && g_stats_prof_on != 0;
+    long long tp[8];
+    tp[0] = prof ? clock64() : 0;
+#define SALE_PHASE(n) \
+    if (prof) tp[n] = clock64();
     const int64_t i = blockIdx.x + 3;
     const int64_t h = blockIdx.y;
     const int64_t b = blockIdx.z;
@@ -111,6 +126,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    SALE_PHASE(1)
 
     // ---- fp32 logits: thread = 4 rows x 14 keys (kg + 16 j), sequential over c;
     //      key pairs (kg + 32p, kg + 32p + 16) share one FFMA2.
@@ -153,6 +169,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
             }
         }
         __syncthreads(); // staging area becomes the logit buffer
+        SALE_PHASE(2)
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -164,6 +181,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
             }
     }
     __syncthreads();
+    SALE_PHASE(3)
 
     // ---- (row, block) tasks: block max
     for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
@@ -175,6 +193,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         sm.bmax[r][s] = bm;
     }
     __syncthreads();
+    SALE_PHASE(4)
     if (tid < kRows) { // running max after each block, in I_SL order
         double m = -INFINITY;
         for (int s = 0; s < nsl; ++s) {
@@ -183,6 +202,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         }
     }
     __syncthreads();
+    SALE_PHASE(5)
     // ---- (row, block) tasks: sequential double sum of exp(s_t - m_new)
     for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
         const int r = task % kRows, s = task / kRows;
@@ -194,6 +214,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         sm.bsum[r][s] = sum;
     }
     __syncthreads();
+    SALE_PHASE(6)
 
     // ---- per row: l = l * exp(m_old - m_new) + sum_b, then the bound
     if (tid < qrows) {
@@ -215,6 +236,13 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
             dbg_bound[o] = bound;
         }
     }
+    if (prof) {
+        tp[7] = clock64();
+        for (int p = 0; p < 7; ++p)
+            atomicAdd(&g_stats_prof[p], static_cast<unsigned long long>(tp[p + 1] - tp[p]));
+        atomicAdd(&g_stats_prof[7], 1ull);
+    }
+#undef SALE_PHASE
 }
 
 // Base mask rows: I_SL U trailing partial run, i.e. {0} U [1 + 4 F_i, frontier]
@@ -274,4 +302,17 @@ cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t 
     return cudaGetLastError();
 }
 
+} // namespace sale_b200
+
+namespace sale_b200 {
+cudaError_t stats_profile(int enable, unsigned long long *out8) {
+    if (out8) {
+        cudaError_t e = cudaMemcpyFromSymbol(out8, g_stats_prof, sizeof(g_stats_prof));
+        if (e != cudaSuccess) return e;
+    }
+    unsigned long long zero[8] = {};
+    cudaError_t e = cudaMemcpyToSymbol(g_stats_prof, zero, sizeof(zero));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(g_stats_prof_on, &enable, sizeof(int));
+}
 } // namespace sale_b200

@@ -19,7 +19,7 @@ ctx = sale.context()
 lib = ctx.lib
 lib.sale_b200_estimator_profile.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
 sale.selection_pass(q, k, qc, qs, kc, ks, 0.004)
-cnt = (C.c_uint64 * 8)()
+cnt = (C.c_uint64 * 16)()
 lib.sale_b200_estimator_profile(ctx.handle, 1, None)
 sale.selection_pass(q, k, qc, qs, kc, ks, 0.004)
 lib.sale_b200_estimator_profile(ctx.handle, 0, cnt)
@@ -30,3 +30,9 @@ print(f"MMA issuer: loop {loop/stages:.0f} cyc/stage; A wait {wa/loop*100:.1f}%,
       f"(ideal MMA time 1024 cyc/stage)")
 print(f"epilogue (warp 4): loop {eloop/stages:.0f} cyc/stage; accumulator-full wait "
       f"{ew/eloop*100:.1f}%")
+st = c[8:16]
+if st[7]:
+    names = ["staging", "dots", "logit store", "block max", "running max", "exp sums", "combine"]
+    tot = sum(st[:7])
+    print("stats kernel (thread 0, per CTA): " + ", ".join(
+        f"{n} {v / st[7]:.0f} cyc ({100 * v / tot:.0f}%)" for n, v in zip(names, st[:7])))
