@@ -51,6 +51,7 @@ struct EstSmem {
     uint64_t tmem_empty[kEstHeads];
     uint32_t tmem_base;
     uint32_t seg_bits[kEstHeads][2][kSegWords];
+    float ks[kSegment * kSegPerUnit];
 };
 
 // Optional wait-time instrumentation (sale_b200_est_profile): cycles the MMA
@@ -189,6 +190,11 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         }
         const float *ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
         const int64_t jb_base = key_base / kBlockK;
+        // the unit's key-block scales, staged once (no global load per stage)
+        for (int x = threadIdx.x - 128; x < kSegment * nstages; x += 32 * kEpiWarps)
+            sm.ks[x] = ks_row[jb_base + x];
+        named_bar_sync(1, 32 * kEpiWarps);
+        const bool dbg = dbg_max != nullptr && row_ok;
         const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 32 * chunk;
         const bool prof = ew == 0 && g_est_prof_on != 0;
         long long w_epi = 0;
@@ -201,9 +207,10 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
 #pragma unroll
             for (int w = 0; w < kSegWords; ++w) flags[hh][w] = 0u;
         for (int k = 0; k < nstages; ++k) {
-            const float ks = ks_row[jb_base + 4 * k + chunk];
+            const float ks = sm.ks[4 * k + chunk];
             const uint32_t kbit = 1u << (k & 31);
-            const int kw = k >> 5;
+            const uint32_t kb0 = (k >> 5) == 0 ? kbit : 0u, kb1 = kbit ^ kb0;
+            static_assert(kSegWords == 2, "flag words");
             // two heads per step: one tcgen05.wait::ld, two independent reductions
 #pragma unroll
             for (int hp = 0; hp < kEstHeads; hp += 2) {
@@ -237,12 +244,10 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                     const int mx = lo > hi ? lo : hi;
                     const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
                     const float est = __fmul_rn(rs, static_cast<float>(mx));
-                    if (est >= fb[hh]) {
-#pragma unroll
-                        for (int w = 0; w < kSegWords; ++w)
-                            if (w == kw) flags[hh][w] |= kbit;
-                    }
-                    if (dbg_max != nullptr && row_ok)
+                    const bool pass = est >= fb[hh];
+                    flags[hh][0] |= pass ? kb0 : 0u;
+                    flags[hh][1] |= pass ? kb1 : 0u;
+                    if (dbg)
                         dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
                                 jb_base + 4 * k + chunk] = mx;
                 }

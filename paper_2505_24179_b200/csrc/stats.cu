@@ -16,9 +16,9 @@
 // is exactly equivalent to the reference's (double)est >= bound.
 //
 // CTA = one (batch, head, query block i >= 3): 64 rows x <= 224 keys x d.
-// Q and the I_SL keys are staged as bf16 with cp.async into rows padded to
-// 264 B (66 words: 16 consecutive rows hit 16 distinct banks). ~72 KB smem,
-// two CTAs per SM.
+// Q and the I_SL keys are staged as bf16 with 16-byte cp.async into rows
+// padded to 272 B (68 words: at most 2-way bank conflicts for the 16 key rows
+// a warp reads). ~75 KB smem, two CTAs per SM.
 #include "common.cuh"
 
 #include <cfloat>
@@ -31,7 +31,7 @@ constexpr int kThreads = 256;
 constexpr int kMaxSlBlocks = 7;                  // {0} U [2i-4, 2i+1]
 constexpr int kMaxKeys = kMaxSlBlocks * kBlockK; // 224
 constexpr int kRows = kBlockQ;                   // 64
-constexpr int kPitch = 132;                      // bf16 per staged row (264 B)
+constexpr int kPitch = 136;                      // bf16 per staged row (272 B, 16-B aligned)
 
 struct StatsSmem {
     union {
@@ -46,10 +46,10 @@ struct StatsSmem {
     int blk_len[kMaxSlBlocks];
 };
 
-__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool valid) {
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
     const uint32_t d = smem_u32(dst);
-    const int n = valid ? 8 : 0; // src-size 0 -> zero fill
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+    const int n = valid ? 16 : 0; // src-size 0 -> zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ void ffma2(unsigned long long &acc, unsigned long long a,
@@ -110,19 +110,20 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
 
     // ---- stage Q rows and I_SL keys (bf16) with cp.async, zero-filling
     //      rows past the sequence end.
-    for (int idx = tid; idx < kRows * (kHeadDim / 4); idx += kThreads) {
-        const int r = idx / (kHeadDim / 4), ch = idx % (kHeadDim / 4);
+    constexpr int kCh = kHeadDim / 8; // 16-byte chunks per row
+    for (int idx = tid; idx < kRows * kCh; idx += kThreads) {
+        const int r = idx / kCh, ch = idx % kCh;
         const bool ok = r < qrows;
-        const __nv_bfloat16 *src = q + ((b * tokens + q0 + (ok ? r : 0)) * hq + h) * kHeadDim + 4 * ch;
-        cp_async8(&sm.u.in.q[r][4 * ch], src, ok);
+        const __nv_bfloat16 *src = q + ((b * tokens + q0 + (ok ? r : 0)) * hq + h) * kHeadDim + 8 * ch;
+        cp_async16(&sm.u.in.q[r][8 * ch], src, ok);
     }
-    for (int idx = tid; idx < kMaxKeys * (kHeadDim / 4); idx += kThreads) {
-        const int t = idx / (kHeadDim / 4), ch = idx % (kHeadDim / 4);
+    for (int idx = tid; idx < kMaxKeys * kCh; idx += kThreads) {
+        const int t = idx / kCh, ch = idx % kCh;
         const int slot = t / kBlockK;
         const int64_t tok = slot < nsl ? slot_token(slot) + t % kBlockK : tokens;
         const bool ok = tok < tokens;
-        const __nv_bfloat16 *src = k + ((b * tokens + (ok ? tok : 0)) * hkv + g) * kHeadDim + 4 * ch;
-        cp_async8(&sm.u.in.k[t][4 * ch], src, ok);
+        const __nv_bfloat16 *src = k + ((b * tokens + (ok ? tok : 0)) * hkv + g) * kHeadDim + 8 * ch;
+        cp_async16(&sm.u.in.k[t][8 * ch], src, ok);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
@@ -208,9 +209,22 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         const int r = task % kRows, s = task / kRows;
         if (s >= nsl) continue;
         const double m_new = sm.bmax[r][s];
+        const float *lg = &sm.u.logit[r][s * kBlockK];
         double sum = 0.0;
-        for (int t = 0; t < sm.blk_len[s]; ++t)
-            sum = __dadd_rn(sum, exp(static_cast<double>(sm.u.logit[r][s * kBlockK + t]) - m_new));
+        if (sm.blk_len[s] == kBlockK) {
+            // independent exps first (ILP), then the reference's sequential sum
+#pragma unroll
+            for (int t0 = 0; t0 < kBlockK; t0 += 8) {
+                double e[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) e[t] = exp(static_cast<double>(lg[t0 + t]) - m_new);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) sum = __dadd_rn(sum, e[t]);
+            }
+        } else {
+            for (int t = 0; t < sm.blk_len[s]; ++t)
+                sum = __dadd_rn(sum, exp(static_cast<double>(lg[t]) - m_new));
+        }
         sm.bsum[r][s] = sum;
     }
     __syncthreads();
