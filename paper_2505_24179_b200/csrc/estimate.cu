@@ -195,6 +195,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             sm.ks[x] = ks_row[jb_base + x];
         named_bar_sync(1, 32 * kEpiWarps);
         const bool dbg = dbg_max != nullptr && row_ok;
+        const bool epi_skip = g_est_prof_on == 2;
         const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 32 * chunk;
         const bool prof = ew == 0 && g_est_prof_on != 0;
         long long w_epi = 0;
@@ -221,6 +222,15 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 if (two) mbar_wait(&sm.tmem_full[hp + 1], k & 1);
                 if (prof) w_epi += clock64() - t0;
                 tc_fence_after();
+                if (epi_skip) { // diagnostic (profile mode 2): MMA side alone
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&sm.tmem_empty[hp]);
+                        if (two) mbar_arrive(&sm.tmem_empty[hp + 1]);
+                    }
+                    continue;
+                }
                 uint32_t v[2][16];
                 tmem_ld32_pack16(acc + 128 * hp, v[0]);
                 if (two) tmem_ld32_pack16(acc + 128 * (hp + 1), v[1]);

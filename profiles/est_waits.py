@@ -36,3 +36,10 @@ if st[7]:
     tot = sum(st[:7])
     print("stats kernel (thread 0, per CTA): " + ", ".join(
         f"{n} {v / st[7]:.0f} cyc ({100 * v / tot:.0f}%)" for n, v in zip(names, st[:7])))
+# mode 2: epilogue skips its TMEM loads and math (MMA / TMA side alone)
+lib.sale_b200_estimator_profile(ctx.handle, 2, None)
+sale.selection_pass(q, k, qc, qs, kc, ks, 0.004)
+lib.sale_b200_estimator_profile(ctx.handle, 0, cnt)
+c = list(cnt)
+print(f"[epilogue work skipped] MMA issuer loop {c[0]/c[4]:.0f} cyc/stage; K-stage wait "
+      f"{c[2]/c[0]*100:.1f}%, accumulator wait {c[3]/c[0]*100:.1f}%")
