@@ -262,10 +262,9 @@ int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *
         mark(ctx, 4, stream);
         return SALE_B200_OK;
     }
-    CUtensorMap tm_qc, tm_kc;
-    if ((st = make_map(ctx, &tm_qc, q_codes, false, s.batch, s.tokens, s.q_heads, 128, 128))) return st;
+    CUtensorMap tm_kc;
     if ((st = make_map(ctx, &tm_kc, k_codes, false, s.batch, s.tokens, s.kv_heads, 128, 128))) return st;
-    SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_units, ctx->n_units, q_scales, k_scales,
+    SALE_CUDA(ctx, launch_estimate(tm_kc, q_codes, ctx->d_units, ctx->n_units, q_scales, k_scales,
                                    thresh, mask, s.batch, s.tokens, static_cast<int>(s.q_heads),
                                    static_cast<int>(s.kv_heads), isd,
                                    dbg ? dbg->block_max : nullptr, stream));

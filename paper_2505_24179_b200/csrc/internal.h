@@ -29,7 +29,7 @@ cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t 
 size_t estimate_smem_bytes();
 cudaError_t estimate_profile(int enable, unsigned long long *out8);
 cudaError_t stats_profile(int enable, unsigned long long *out8);
-cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
+cudaError_t launch_estimate(const CUtensorMap &tm_kc, const int8_t *q_codes, const EstUnit *units,
                             int64_t n_units, const float *q_scales, const float *k_scales,
                             const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
                             int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
