@@ -262,9 +262,10 @@ int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *
         mark(ctx, 4, stream);
         return SALE_B200_OK;
     }
-    CUtensorMap tm_kc;
+    CUtensorMap tm_qc, tm_kc;
+    if ((st = make_map(ctx, &tm_qc, q_codes, false, s.batch, s.tokens, s.q_heads, 128, 128))) return st;
     if ((st = make_map(ctx, &tm_kc, k_codes, false, s.batch, s.tokens, s.kv_heads, 128, 128))) return st;
-    SALE_CUDA(ctx, launch_estimate(tm_kc, q_codes, ctx->d_units, ctx->n_units, q_scales, k_scales,
+    SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_units, ctx->n_units, q_scales, k_scales,
                                    thresh, mask, s.batch, s.tokens, static_cast<int>(s.q_heads),
                                    static_cast<int>(s.kv_heads), isd,
                                    dbg ? dbg->block_max : nullptr, stream));
@@ -276,11 +277,12 @@ int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void 
                    const sale_b200_shape &s, const uint32_t *mask, void *out, int32_t *coverage,
                    cudaStream_t stream) {
     int st;
-    CUtensorMap tk, tv;
+    CUtensorMap tq, tk, tv;
+    if ((st = make_map(ctx, &tq, q, true, s.batch, s.tokens, s.q_heads, 64, 64))) return st;
     if ((st = make_map(ctx, &tk, k, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
     if ((st = make_map(ctx, &tv, v, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
     const float scale_log2 = inv_sqrt_dim(s.head_dim) * 1.4426950408889634f;
-    SALE_CUDA(ctx, launch_sparse_attention(q, tk, tv, mask, out, coverage, s.batch, s.tokens,
+    SALE_CUDA(ctx, launch_sparse_attention(tq, tk, tv, mask, out, coverage, s.batch, s.tokens,
                                            static_cast<int>(s.q_heads), static_cast<int>(s.kv_heads),
                                            scale_log2, stream));
     mark(ctx, 5, stream);

@@ -9,23 +9,21 @@
 // x one 128-row query tile x a chunk of up to kSegPerUnit middle segments.
 //   * The 128-row tile pairs query blocks (2m+1, 2m+2): both have the same
 //     full-segment count F = m-1, so one key range
-//     serves both.
-//   * A = the 4 heads' Q codes (4 x 128 rows x 128 int8) is written once into
-//     TMEM columns [0, 128) and every MMA reads it from there: only K codes
-//     stream from shared memory (64 B/clk at full MMA rate instead of 128 —
-//     with both operands in SMEM the port, not the tensor core, paced the MMA).
+//     serves both. A = 4 heads x [128 rows x 128 int8 codes] (64 KB) is loaded
+//     once by TMA.
 //   * One stage = one segment = 128 keys (16 KB) through a 6-deep TMA ring.
-//     Every tcgen05.mma is M=128, N=128, K=32 (profiles/r1_mma_microbench.txt:
-//     an MMA costs >= 46 cycles whatever its N; at N=128 i8 runs at
-//     8192 MAC/clk/SM). A stage = 4 heads x 4 K-steps; head-step g writes
-//     accumulator buffer g % 3 (three 128-column buffers in [128, 512)).
+//     Every tcgen05.mma has N = 128 (profiles/r1_mma_microbench.txt: an MMA
+//     instruction costs >= 46 cycles whatever its N, so N = 32/64 tiles waste
+//     the tensor core; at N >= 128 i8 runs at 8192 MAC/clk/SM).
+//   * TMEM holds one 128-column accumulator per head; a stage is 4 heads x 4
+//     K-steps of M=128, N=128, K=32, head h into buffer h, so head h's epilogue
+//     has the other three heads' MMAs to drain its buffer, and each K-code
+//     stage is shared by 4 heads (M = 512 rows per byte of K).
 //   * Epilogue (16 warps = 4 lane quadrants x 4 key blocks, thread = row):
-//     per head-step one tcgen05.ld .pack::16b (|products| <= 128*49 fits
-//     int16), release of the buffer, 16-bit SIMD max, then
-//     est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max >= fb_row — the
-//     reference's float arithmetic. Per-row flags are kept as bitmasks over the
-//     unit's segments and OR-reduced over rows once (redux), then OR-ed into
-//     the packed mask with atomicOr.
+//     tcgen05.ld .pack::16b (|products| <= 128*49 fits int16), 16-bit SIMD max
+//     per 32-key block, est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max,
+//     est >= fb_row — the reference's float arithmetic. A warp vote ORs rows,
+//     atomicOr ORs segments into the packed mask.
 #include "common.cuh"
 #include "internal.h"
 
@@ -36,38 +34,36 @@ constexpr int kSegWords = kSegPerUnit / 32;
 constexpr int kEstHeads = 4;               // query heads per CTA
 constexpr int kEstStages = 6;              // TMA ring depth
 constexpr int kStageKeys = kSegment * kBlockK;       // 128 keys = one segment
+constexpr int kATileBytes = 128 * kHeadDim;          // 16 KB per head
 constexpr int kBStageBytes = kStageKeys * kHeadDim;  // 16 KB
-constexpr int kAccBufs = 3;                // rotating 128-column accumulators
-constexpr uint32_t kColAcc = 128;          // TMEM: A [0,128) | acc [128,512)
-constexpr int kEpiWarps = 16;              // (lane quadrant, key block) per warp
+constexpr int kEpiWarps = 16;              // one (lane quadrant, query head) per warp
 constexpr int kEstThreads = 128 + 32 * kEpiWarps; // warps 0-3 control, 4-19 epilogue
 
 static_assert(kSegPerUnit == kSegPerUnitHost, "unit size mismatch");
-static_assert(kSegWords == 2, "flag words");
 
 struct EstSmem {
+    alignas(1024) uint8_t a[kEstHeads][kATileBytes];
     alignas(1024) uint8_t bst[kEstStages][kBStageBytes];
     uint64_t full[kEstStages];
     uint64_t empty[kEstStages];
-    uint64_t a_ready;
-    uint64_t tmem_full[kAccBufs];
-    uint64_t tmem_empty[kAccBufs];
+    uint64_t a_full;
+    uint64_t tmem_full[kEstHeads];
+    uint64_t tmem_empty[kEstHeads];
     uint32_t tmem_base;
     uint32_t seg_bits[kEstHeads][2][kSegWords];
     float ks[kSegment * kSegPerUnit];
 };
 
-// Optional wait-time instrumentation (sale_b200_estimator_profile): cycles the
-// MMA issuer spends blocked on K stages / accumulator buffers, and the epilogue
-// on accumulators. Off unless enabled; one global flag read per CTA. Mode 2
-// additionally skips the epilogue's loads and math (diagnostic).
+// Optional wait-time instrumentation (sale_b200_est_profile): cycles the MMA
+// issuer spends blocked on K stages / accumulator buffers, and the epilogue on
+// accumulators. Off unless enabled; one global flag read per CTA.
 __device__ int g_est_prof_on = 0;
 __device__ unsigned long long g_est_prof[8];
 
 namespace {
 
 __global__ void __launch_bounds__(kEstThreads, 1)
-estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restrict__ q_codes,
+estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_kc,
                 const EstUnit *__restrict__ units, const float *__restrict__ q_scales,
                 const float *__restrict__ k_scales, const float *__restrict__ thresh,
                 uint32_t *__restrict__ mask, int64_t tokens, int hq, int hkv, int nsub,
@@ -93,17 +89,16 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
     const int nstages = u.nseg;
     const int row0 = 128 * u.m + 64;
     const int key_base = kBlockK + kStageKeys * kSegPerUnit * u.c; // first key of the unit
-    const int64_t jb_base = key_base / kBlockK;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kEstStages; ++s) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], 1);
         }
-        mbar_init(&sm.a_ready, kEpiWarps);
-        for (int s = 0; s < kAccBufs; ++s) {
+        mbar_init(&sm.a_full, 1);
+        for (int s = 0; s < kEstHeads; ++s) {
             mbar_init(&sm.tmem_full[s], 1);
-            mbar_init(&sm.tmem_empty[s], kEpiWarps);
+            mbar_init(&sm.tmem_empty[s], kEpiWarps); // all epilogue warps drain every group
         }
         for (int hh = 0; hh < kEstHeads; ++hh)
             for (int x = 0; x < 2; ++x)
@@ -119,7 +114,11 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
     if (warp == 0) {
         // ---------------------------------------------------------- TMA producer
         if (elect_one()) {
+            tma_prefetch(&tm_qc);
             tma_prefetch(&tm_kc);
+            mbar_expect_tx(&sm.a_full, static_cast<uint32_t>(nh * kATileBytes));
+            for (int hh = 0; hh < nh; ++hh)
+                tma_load_4d(sm.a[hh], &tm_qc, &sm.a_full, 0, h0 + hh, row0, b);
             for (int k = 0; k < nstages; ++k) {
                 const int st = k % kEstStages;
                 mbar_wait(&sm.empty[st], ((k / kEstStages) & 1) ^ 1);
@@ -131,29 +130,32 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
         // ------------------------------------------------------------ MMA issuer
         if (elect_one()) {
             constexpr uint32_t idesc = idesc_i8(128, kStageKeys);
+            uint64_t adesc[kEstHeads];
+            for (int hh = 0; hh < kEstHeads; ++hh)
+                adesc[hh] = umma_desc_sw128(smem_u32(sm.a[hh]), 16, 1024);
             const bool prof = g_est_prof_on != 0;
             long long t_start = clock64(), w_full = 0, w_empty = 0;
-            mbar_wait(&sm.a_ready, 0);
+            mbar_wait(&sm.a_full, 0);
             const long long w_a = clock64() - t_start;
             tc_fence_after();
-            int step = 0; // head-steps issued
             for (int k = 0; k < nstages; ++k) {
                 const int st = k % kEstStages;
                 long long t0 = prof ? clock64() : 0;
                 mbar_wait(&sm.full[st], (k / kEstStages) & 1);
                 if (prof) w_full += clock64() - t0;
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.bst[st]), 16, 1024);
-                for (int hh = 0; hh < nh; ++hh, ++step) {
-                    const int bb = step % kAccBufs;
+                for (int hh = 0; hh < nh; ++hh) {
+                    // head hh owns TMEM columns [128 hh, 128 hh + 128): its
+                    // epilogue of stage k-1 had three other heads' MMAs to finish
                     t0 = prof ? clock64() : 0;
-                    mbar_wait(&sm.tmem_empty[bb], ((step / kAccBufs) & 1) ^ 1);
+                    mbar_wait(&sm.tmem_empty[hh], (k & 1) ^ 1);
                     if (prof) w_empty += clock64() - t0;
                     tc_fence_after();
-                    const uint32_t d = tmem + kColAcc + 128 * bb;
+                    const uint32_t d = tmem + 128 * hh;
 #pragma unroll
-                    for (int kk = 0; kk < kHeadDim / 32; ++kk) // K = 32 int8 = 8 TMEM columns
-                        mma_i8_ts(d, tmem + 32 * hh + 8 * kk, bdesc + 2 * kk, idesc, kk > 0);
-                    tc_commit(&sm.tmem_full[bb]);
+                    for (int kk = 0; kk < kHeadDim / 32; ++kk)
+                        mma_i8_ss(d, adesc[hh] + 2 * kk, bdesc + 2 * kk, idesc, kk > 0);
+                    tc_commit(&sm.tmem_full[hh]);
                 }
                 tc_commit(&sm.empty[st]);
             }
@@ -172,30 +174,9 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
         const int r = quad * 32 + lane;       // row within the 128-row tile
         const int64_t tok = row0 + r;
         const bool row_ok = tok < tokens;
-        const int chunk = ew >> 2;            // key block of the segment (32 columns)
-        const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        // A operand: head `chunk`'s codes of this row -> TMEM columns [32 chunk, +32)
-        if (chunk < nh) {
-            uint32_t a[32];
-            if (row_ok) {
-                const uint4 *src = reinterpret_cast<const uint4 *>(
-                    q_codes + ((static_cast<int64_t>(b) * tokens + tok) * hq + h0 + chunk) * kHeadDim);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint4 w = __ldg(src + e);
-                    a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 32; ++e) a[e] = 0u;
-            }
-            tmem_st32(lane_addr + 32 * chunk, a);
-            tmem_st_wait();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.a_ready);
-
+        // Every head's buffer is drained by all 16 warps: warp = (quadrant,
+        // key block `chunk` of the segment = 32 accumulator columns).
+        const int chunk = ew >> 2;
         float qs[kEstHeads], fb[kEstHeads];
 #pragma unroll
         for (int hh = 0; hh < kEstHeads; ++hh) {
@@ -207,13 +188,15 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
                 fb[hh] = thresh[o];
             }
         }
-        // the unit's key-block scales, staged once (no global load per stage)
         const float *ks_row = k_scales + (static_cast<int64_t>(b) * hkv + g) * nk;
+        const int64_t jb_base = key_base / kBlockK;
+        // the unit's key-block scales, staged once (no global load per stage)
         for (int x = threadIdx.x - 128; x < kSegment * nstages; x += 32 * kEpiWarps)
             sm.ks[x] = ks_row[jb_base + x];
         named_bar_sync(1, 32 * kEpiWarps);
         const bool dbg = dbg_max != nullptr && row_ok;
         const bool epi_skip = g_est_prof_on == 2;
+        const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 32 * chunk;
         const bool prof = ew == 0 && g_est_prof_on != 0;
         long long w_epi = 0;
         const long long t_epi = clock64();
@@ -221,46 +204,63 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_kc, const int8_t *__restr
         // this row's key block in segment k passed; OR-reduced over rows once
         uint32_t flags[kEstHeads][kSegWords];
 #pragma unroll
-        for (int hh = 0; hh < kEstHeads; ++hh) flags[hh][0] = flags[hh][1] = 0u;
-        int step = 0;
+        for (int hh = 0; hh < kEstHeads; ++hh)
+#pragma unroll
+            for (int w = 0; w < kSegWords; ++w) flags[hh][w] = 0u;
         for (int k = 0; k < nstages; ++k) {
             const float ks = sm.ks[4 * k + chunk];
             const uint32_t kbit = 1u << (k & 31);
             const uint32_t kb0 = (k >> 5) == 0 ? kbit : 0u, kb1 = kbit ^ kb0;
+            static_assert(kSegWords == 2, "flag words");
+            // two heads per step: one tcgen05.wait::ld, two independent reductions
 #pragma unroll
-            for (int hh = 0; hh < kEstHeads; ++hh) {
-                if (hh >= nh) break; // warp-uniform
-                const int bb = step % kAccBufs;
-                const uint32_t ph = (step / kAccBufs) & 1;
-                ++step;
+            for (int hp = 0; hp < kEstHeads; hp += 2) {
+                if (hp >= nh) break; // warp-uniform
+                const bool two = hp + 1 < nh;
                 const long long t0 = prof ? clock64() : 0;
-                mbar_wait(&sm.tmem_full[bb], ph);
+                mbar_wait(&sm.tmem_full[hp], k & 1);
+                if (two) mbar_wait(&sm.tmem_full[hp + 1], k & 1);
                 if (prof) w_epi += clock64() - t0;
                 tc_fence_after();
-                uint32_t v[16];
-                if (!epi_skip) {
-                    tmem_ld32_pack16(lane_addr + kColAcc + 128 * bb + 32 * chunk, v);
-                    tmem_ld_wait();
+                if (epi_skip) { // diagnostic (profile mode 2): MMA side alone
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&sm.tmem_empty[hp]);
+                        if (two) mbar_arrive(&sm.tmem_empty[hp + 1]);
+                    }
+                    continue;
                 }
+                uint32_t v[2][16];
+                tmem_ld32_pack16(acc + 128 * hp, v[0]);
+                if (two) tmem_ld32_pack16(acc + 128 * (hp + 1), v[1]);
+                tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.tmem_empty[bb]); // registers hold the data
-                if (epi_skip) continue;
+                if (lane == 0) { // registers hold the data now: release the buffers
+                    mbar_arrive(&sm.tmem_empty[hp]);
+                    if (two) mbar_arrive(&sm.tmem_empty[hp + 1]);
+                }
 #pragma unroll
-                for (int s = 8; s > 0; s >>= 1)
+                for (int x = 0; x < 2; ++x) {
+                    if (x == 1 && !two) break;
+                    const int hh = hp + x;
 #pragma unroll
-                    for (int e = 0; e < s; ++e) v[e] = __vmaxs2(v[e], v[e + s]);
-                const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
-                const int hi = static_cast<int16_t>(v[0] >> 16);
-                const int mx = lo > hi ? lo : hi;
-                const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
-                const float est = __fmul_rn(rs, static_cast<float>(mx));
-                const bool pass = est >= fb[hh];
-                flags[hh][0] |= pass ? kb0 : 0u;
-                flags[hh][1] |= pass ? kb1 : 0u;
-                if (dbg)
-                    dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                            jb_base + 4 * k + chunk] = mx;
+                    for (int s = 8; s > 0; s >>= 1)
+#pragma unroll
+                        for (int e = 0; e < s; ++e) v[x][e] = __vmaxs2(v[x][e], v[x][e + s]);
+                    const int lo = static_cast<int16_t>(v[x][0] & 0xFFFFu);
+                    const int hi = static_cast<int16_t>(v[x][0] >> 16);
+                    const int mx = lo > hi ? lo : hi;
+                    const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
+                    const float est = __fmul_rn(rs, static_cast<float>(mx));
+                    const bool pass = est >= fb[hh];
+                    flags[hh][0] |= pass ? kb0 : 0u;
+                    flags[hh][1] |= pass ? kb1 : 0u;
+                    if (dbg)
+                        dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                                jb_base + 4 * k + chunk] = mx;
+                }
             }
         }
         // OR over the warp's 32 rows; the two query blocks of the tile are the
@@ -320,7 +320,7 @@ cudaError_t estimate_profile(int enable, unsigned long long *out8) {
     return cudaMemcpyToSymbol(g_est_prof_on, &enable, sizeof(int));
 }
 
-cudaError_t launch_estimate(const CUtensorMap &tm_kc, const int8_t *q_codes, const EstUnit *units,
+cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
                             int64_t n_units, const float *q_scales, const float *k_scales,
                             const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
                             int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
@@ -338,7 +338,7 @@ cudaError_t launch_estimate(const CUtensorMap &tm_kc, const int8_t *q_codes, con
     const int group = hq / hkv;
     const int nsub = (group + kEstHeads - 1) / kEstHeads;
     dim3 grid(static_cast<unsigned>(n_units), static_cast<unsigned>(batch * hkv * nsub));
-    estimate_kernel<<<grid, kEstThreads, smem, stream>>>(tm_kc, q_codes, units, q_scales, k_scales,
+    estimate_kernel<<<grid, kEstThreads, smem, stream>>>(tm_qc, tm_kc, units, q_scales, k_scales,
                                                          thresh, mask, tokens, hq, hkv, nsub,
                                                          inv_sqrt_d, dbg_max);
     return cudaGetLastError();

@@ -29,17 +29,17 @@ cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t 
 size_t estimate_smem_bytes();
 cudaError_t estimate_profile(int enable, unsigned long long *out8);
 cudaError_t stats_profile(int enable, unsigned long long *out8);
-cudaError_t launch_estimate(const CUtensorMap &tm_kc, const int8_t *q_codes, const EstUnit *units,
+cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
                             int64_t n_units, const float *q_scales, const float *k_scales,
                             const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
                             int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
                             cudaStream_t stream);
 
 size_t attention_smem_bytes();
-cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
-                                    const uint32_t *mask, void *out, int32_t *coverage,
-                                    int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
-                                    cudaStream_t stream);
+cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &tm_k,
+                                    const CUtensorMap &tm_v, const uint32_t *mask, void *out,
+                                    int32_t *coverage, int64_t batch, int64_t tokens, int hq,
+                                    int hkv, float scale_log2, cudaStream_t stream);
 
 cudaError_t launch_flop_count(const uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
                               int64_t *counts, cudaStream_t stream);
