@@ -8,49 +8,48 @@
 // t contributes to row g iff t <= g and mask(qblock(g), kblock(t)) is set;
 // fully-future mask bits are ignored; coverage[g] counts the attended tokens.
 //
-// CTA = one query block i (64 tokens) of FOUR query heads of one GQA group, as
-// two M=128 tiles: tile A = heads (h, h+1), tile B = heads (h+2, h+3) (rows
-// 0-63 / 64-127 of a tile are the two heads). All four heads need the same
-// K/V and causal extent. Key tiles follow the segment grid of the
-// Selection-Pass: tile 0 = the 32-key sink block, tile s+1 = keys
-// [32+128s, 160+128s) = key blocks 1+4s..4+4s. K/V of a key tile are loaded
-// once if any of the 16 (head, key block) bits is set; each M=128 tile issues
-// its MMAs only if one of its 8 bits is set; inside a tile unselected 32-key
-// sub-blocks and the causal diagonal are masked per row.
+// CTA = one query block i (64 tokens) of TWO query heads of the same GQA group
+// (rows 0-63 head 2p, rows 64-127 head 2p+1): both halves need exactly the same
+// K/V and the same causal extent, and per-head masks of one query block
+// overlap more than masks of adjacent query blocks (profiles/mask_stats.py).
+// Key tiles follow the segment grid of the Selection-Pass: tile 0 = the
+// 32-key sink block, tile s+1 = keys [32+128s, 160+128s) = key blocks
+// 1+4s..4+4s. A tile is visited iff any of its 8 (head, kblock) bits is set;
+// inside a visited tile unselected 32-key sub-blocks and the causal diagonal
+// are masked per row.
 //
-// TMEM (512 columns): O_A [0,128) | O_B [128,256) | S_A [256,384) | S_B
-// [384,512); P overwrites S in place as the A operand of O += P V.
+// TMEM (512 columns): O [0,128) | S0 [128,256) | S1 [256,384) | Q [384,448).
+// Q sits in TMEM as the A operand of S = Q K^T (only K streams from shared
+// memory; with A in SMEM an M=N=128 bf16 MMA needs the full 128 B/clk port),
+// and P overwrites S in place as the A operand of O += P V.
 //
-// Pipeline (FA4-style ping-pong, one elected thread per role):
-//   warp 0  TMA: Q_A, Q_B once, then K_j, V_j into a 2-stage ring (SW128)
-//   warp 1  MMA: per key tile j:  O_A += P_A(j-1) V_{j-1};  S_A = Q_A K_j;
-//                                 O_B += P_B(j-1) V_{j-1};  S_B = Q_B K_j
-//           so softmax A works on S_A(j) while the tensor core runs tile B
-//   warps 4-7 softmax of tile A, warps 8-11 of tile B (thread = row): mask,
-//           lazy-rescaled exp2-domain online softmax (O rescaled in TMEM only
-//           when the running max grows by > 8), MUFU + FMA-polynomial exp2,
+// Pipeline (warp-specialised, one elected thread per role):
+//   warp 0  TMA: K_j, V_j into a 3-stage ring (SW128 tiles)
+//   warp 1  MMA: S_j = Q K_j^T into TMEM buffer j%2 (8 x K=16), then
+//           O += P_{j-1} V_{j-1}
+//   warps 4-7  softmax, thread = row: Q row -> TMEM once; per tile tcgen05.ld S
+//           row, mask, lazy-rescaled online softmax in the exp2 domain (O
+//           rescaled in TMEM only when the running max grows by > 8),
 //           P -> bf16 -> tcgen05.st over S.
 #include "common.cuh"
 
 namespace sale_b200 {
 
-constexpr int kAttnThreads = 384;
+constexpr int kAttnThreads = 256;
 constexpr int kMaxTiles = 4200;                // supports N <= 512K
-constexpr int kKvStages = 2;
+constexpr int kKvStages = 3;
 constexpr int kTileBytesHalf = 128 * 64 * 2;   // 128 rows x 64 bf16 = 16 KB
-constexpr uint32_t kColO = 0, kColS = 256;     // O_X at 128 X, S_X at 256 + 128 X
-constexpr int kTileBits = 13;                  // tiles[] = j | bits16 << 13
+constexpr uint32_t kColO = 0, kColS0 = 128, kColQ = 384;
 
 struct AttnSmem {
-    alignas(1024) uint8_t q[2][2][kTileBytesHalf];          // [tile][d half]
     alignas(1024) uint8_t k[kKvStages][2][kTileBytesHalf];
     alignas(1024) uint8_t v[kKvStages][2][kTileBytesHalf];
-    uint64_t q_full, k_full[kKvStages], v_full[kKvStages], kv_empty[kKvStages];
-    uint64_t s_full[2], p_full[2], pv_done[2];              // per M=128 tile
+    uint64_t q_ready, k_full[kKvStages], v_full[kKvStages], kv_empty[kKvStages];
+    uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
     int ntiles;
-    int warp_cnt[12];
-    uint32_t tiles[kMaxTiles];
+    int warp_cnt[8];
+    uint32_t tiles[kMaxTiles]; // j | bits8 << 16
 };
 
 namespace {
@@ -95,8 +94,7 @@ struct SoftmaxState {
 // One S tile of one row (thread): mask, lazy online-softmax update, P -> TMEM.
 // NK = keys in the tile (32 for the sink tile, 128 otherwise). S holds raw
 // fp32 logits*sqrt(d) bits; P (bf16 pairs) is written over the first NK/2
-// columns of the same buffer. Two passes over TMEM in 32-column chunks (max,
-// then exp) keep the live state to one chunk, so two softmax warpgroups fit.
+// columns of the same buffer.
 template <int NK>
 __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uint32_t nib,
                                              int64_t lim, float scale_log2, SoftmaxState &st,
@@ -104,44 +102,39 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
     // The other head of the pair selected this tile, this warp's rows did not
     // (or they are all in the causal future): P = 0, no exp work.
     if (__all_sync(0xffffffffu, nib == 0u || lim < 0)) {
-        uint32_t z[16];
+        uint32_t z[32];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) z[e] = 0u;
-#pragma unroll
-        for (int c4 = 0; c4 < NK / 32; ++c4) tmem_st16(sAddr + 16 * c4, z);
+        for (int e = 0; e < 32; ++e) z[e] = 0u;
+        if constexpr (NK == 128) {
+            tmem_st32(sAddr, z);
+            tmem_st32(sAddr + 32, z);
+        } else {
+            tmem_st16(sAddr, *reinterpret_cast<uint32_t(*)[16]>(&z[0]));
+        }
         tmem_st_wait();
         return;
     }
+    uint32_t s[NK];
+#pragma unroll
+    for (int c4 = 0; c4 < NK / 32; ++c4)
+        tmem_ld32(sAddr + 32 * c4, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c4]));
+    tmem_ld_wait();
     // column c valid iff its 32-key sub-block is selected and c <= lim (causal);
     // fully selected, fully past tiles skip the per-element test.
     const bool full = nib == ((1u << (NK / 32)) - 1u) && lim >= NK - 1;
-    auto masked = [&](uint32_t (&s)[32], int c4) {
-        if (full) return;
-        const bool blk = (nib >> c4) & 1u;
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-            s[c] = (blk && 32 * c4 + c <= lim) ? s[c] : __float_as_uint(-INFINITY);
-    };
-    // pass 1: row max
-    float mt = -INFINITY;
-#pragma unroll
-    for (int c4 = 0; c4 < NK / 32; ++c4) {
-        uint32_t s[32];
-        tmem_ld32(sAddr + 32 * c4, s);
-        tmem_ld_wait();
-        masked(s, c4);
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) mt = fmax3(mt, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
-    }
     int nvalid = NK;
     if (!full) {
         nvalid = 0;
 #pragma unroll
-        for (int c4 = 0; c4 < NK / 32; ++c4) {
-            const int64_t hi = lim - 32 * c4; // valid columns of the chunk: 0 .. min(31, hi)
-            nvalid += ((nib >> c4) & 1u) ? static_cast<int>(hi < 0 ? 0 : (hi > 31 ? 32 : hi + 1)) : 0;
+        for (int c = 0; c < NK; ++c) {
+            const bool ok = ((nib >> (c >> 5)) & 1u) && c <= lim;
+            s[c] = ok ? s[c] : __float_as_uint(-INFINITY);
+            nvalid += ok ? 1 : 0;
         }
     }
+    float mt = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < NK; c += 2) mt = fmax3(mt, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
     const float m_new = fmaxf(st.m_run, mt * scale_log2);
     const bool need = st.m_run != -INFINITY && m_new > st.m_run + 8.0f;
     if (st.m_run == -INFINITY) st.m_run = m_new;
@@ -165,29 +158,21 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
             st.m_run = m_new;
         }
     }
-    // pass 2: p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0.
-    // A row with nothing valid yet keeps m = -inf: use 0 so -inf*scale - 0 = -inf.
-    // P of chunk c4 goes to columns [16 c4, 16 c4 + 16), all already consumed.
+    // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
+    // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
     const float neg_m = st.m_run == -INFINITY ? 0.0f : -st.m_run;
     const unsigned long long sc2 = pack_f2(scale_log2, scale_log2), nm2 = pack_f2(neg_m, neg_m);
-    const bool poly = NK == 128 && __all_sync(0xffffffffu, full);
     unsigned long long psum2 = 0ull;
+    if (NK == 128 && __all_sync(0xffffffffu, full)) {
+        // Full tiles: one pair in four takes exp2 on the FMA pipe (Cody-Waite
+        // split + degree-3 polynomial, rel. err 1e-4 < bf16's 2^-8) so the
+        // MUFU pipe (16 ex2/clk/SM) stops being the co-bottleneck with the MMA.
 #pragma unroll
-    for (int c4 = 0; c4 < NK / 32; ++c4) {
-        uint32_t s[32];
-        tmem_ld32(sAddr + 32 * c4, s);
-        tmem_ld_wait();
-        masked(s, c4);
-        uint32_t pk[16];
-#pragma unroll
-        for (int c2 = 0; c2 < 16; ++c2) {
+        for (int c2 = 0; c2 < NK / 2; ++c2) {
             unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
-            ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
+            ffma2_f32(x, sc2, nm2);
             float p0, p1;
-            if (poly && (c2 & 3) == 3) {
-                // Full tiles: one pair in four takes exp2 on the FMA pipe
-                // (Cody-Waite split + degree-3 polynomial, rel. err 1e-4 < bf16's
-                // 2^-8) so MUFU (16 ex2/clk/SM) stops pacing the tensor core.
+            if ((c2 & 3) == 3) {
                 const unsigned long long xc =
                     pack_f2(fmaxf(__uint_as_float(static_cast<uint32_t>(x)), -125.0f),
                             fmaxf(__uint_as_float(static_cast<uint32_t>(x >> 32)), -125.0f));
@@ -210,18 +195,33 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
                 p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
             }
             fadd2_f32(psum2, pack_f2(p0, p1));
-            pk[c2] = pack_bf16x2(p0, p1);
+            s[c2] = pack_bf16x2(p0, p1);
         }
-        tmem_st16(sAddr + 16 * c4, pk);
+    } else {
+#pragma unroll
+        for (int c2 = 0; c2 < NK / 2; ++c2) {
+            unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
+            ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
+            const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
+            const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
+            fadd2_f32(psum2, pack_f2(p0, p1));
+            s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
+        }
     }
     st.l_run += __uint_as_float(static_cast<uint32_t>(psum2)) +
                 __uint_as_float(static_cast<uint32_t>(psum2 >> 32));
     st.cov += nvalid;
+    if constexpr (NK == 128) {
+        tmem_st32(sAddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_st32(sAddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+    } else {
+        tmem_st16(sAddr, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
+    }
     tmem_st_wait();
 }
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
-sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const uint32_t *__restrict__ mask,
                         __nv_bfloat16 *__restrict__ out, int32_t *__restrict__ coverage,
                         int64_t tokens, int hq, int hkv, float scale_log2) {
@@ -236,23 +236,23 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t words = (nk + 31) / 32;
     // CTA order: (batch, KV head) major, then query blocks heaviest first, then
-    // the head quads of the GQA group — concurrently resident CTAs stream the
+    // the head pairs of the GQA group — concurrently resident CTAs stream the
     // same K/V prefix, so the ~64 MB of K/V per KV head at 128K is read from
     // HBM about once and then served from L2.
     const int group = hq / hkv;
-    const int nquads = (group + 3) / 4;
-    const int qd = static_cast<int>(blockIdx.x % nquads);
-    const int64_t i = nq - 1 - static_cast<int64_t>((blockIdx.x / nquads) % nq);
-    const int bg = static_cast<int>(blockIdx.x / (nquads * nq));
+    const int npairs = (group + 1) / 2;
+    const int p = static_cast<int>(blockIdx.x % npairs);
+    const int64_t i = nq - 1 - static_cast<int64_t>((blockIdx.x / npairs) % nq);
+    const int bg = static_cast<int>(blockIdx.x / (npairs * nq));
     const int g = bg % hkv;
     const int b = bg / hkv;
-    const int hbase = g * group + 4 * qd;             // heads hbase .. hbase+3
-    const int nh = min(4, group - 4 * qd);            // heads present in this quad
+    const int hA = g * group + 2 * p;
+    const bool hasB = 2 * p + 1 < group;
     const int64_t q0 = i * kBlockQ;
     const int64_t qend = q0 + kBlockQ < tokens ? q0 + kBlockQ : tokens;
 
     if (tid == 0) {
-        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.q_ready, 4);
         for (int s = 0; s < kKvStages; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.v_full[s], 1);
@@ -268,8 +268,10 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
     }
     if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
 
-    // ---- active key-tile list (block-wide stream compaction, ascending)
-    const int64_t rowbase = (static_cast<int64_t>(b) * hq + hbase) * nq + i;
+    // ---- active tile list (block-wide stream compaction, ascending order)
+    const int64_t rowbase = (static_cast<int64_t>(b) * hq + hA) * nq + i;
+    const uint32_t *rowA = mask ? mask + rowbase * words : nullptr;
+    const uint32_t *rowB = (mask && hasB) ? mask + (rowbase + nq) * words : nullptr;
     const int total = qend > kBlockK ? 1 + static_cast<int>((qend - kBlockK + 127) / 128) : 1;
     __syncthreads();
     for (int start = 0; start < total; start += kAttnThreads) {
@@ -281,10 +283,9 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
             uint32_t causal = 0; // key blocks that exist and are not fully future
             for (int e = 0; e < nsub; ++e)
                 if (j0 + e < nk && (j0 + e) * kBlockK < qend) causal |= 1u << e;
-            for (int x = 0; x < nh; ++x) {
-                const uint32_t nib = mask ? mask_bits4(mask + (rowbase + x * nq) * words, words, j0) : 0xFu;
-                bits |= (nib & causal) << (4 * x);
-            }
+            const uint32_t nibA = mask ? mask_bits4(rowA, words, j0) : 0xFu;
+            const uint32_t nibB = !hasB ? 0u : (mask ? mask_bits4(rowB, words, j0) : 0xFu);
+            bits = (nibA & causal) | ((nibB & causal) << 4);
         }
         const bool active = bits != 0;
         const uint32_t ballot = __ballot_sync(0xffffffffu, active);
@@ -294,7 +295,7 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
         for (int w = 0; w < warp; ++w) base += sm.warp_cnt[w];
         if (active) {
             const int pos = base + __popc(ballot & ((1u << lane) - 1u));
-            if (pos < kMaxTiles) sm.tiles[pos] = static_cast<uint32_t>(j) | (bits << kTileBits);
+            if (pos < kMaxTiles) sm.tiles[pos] = static_cast<uint32_t>(j) | (bits << 16);
         }
         __syncthreads();
         if (tid == 0) {
@@ -309,24 +310,15 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
     const int ntiles = sm.ntiles;
-    auto need = [&](int jj, int x) -> bool { // tile x (0 = A, 1 = B) needs key tile jj
-        return ((sm.tiles[jj] >> (kTileBits + 8 * x)) & 0xFFu) != 0;
-    };
 
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA
         if (elect_one() && ntiles > 0) {
-            tma_prefetch(&tm_q);
             tma_prefetch(&tm_k);
             tma_prefetch(&tm_v);
-            mbar_expect_tx(&sm.q_full, static_cast<uint32_t>(nh * 2 * (kTileBytesHalf / 2)));
-            for (int x = 0; x < nh; ++x) // head hbase+x -> tile x/2, rows 64 (x&1) ..
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_4d(sm.q[x >> 1][hf] + (x & 1) * (kTileBytesHalf / 2), &tm_q, &sm.q_full,
-                                64 * hf, hbase + x, static_cast<int>(q0), b);
             for (int jj = 0; jj < ntiles; ++jj) {
                 const int st = jj % kKvStages;
-                const int j = static_cast<int>(sm.tiles[jj] & ((1u << kTileBits) - 1u));
+                const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
                 const int key0 = j == 0 ? 0 : kBlockK + 128 * (j - 1);
                 mbar_wait(&sm.kv_empty[st], ((jj / kKvStages) & 1) ^ 1);
                 mbar_expect_tx(&sm.k_full[st], 2 * kTileBytesHalf);
@@ -341,95 +333,99 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
         // ---------------------------------------------------------------- MMA
         if (elect_one() && ntiles > 0) {
             constexpr uint32_t idesc_pv = idesc_bf16(128, 128, true);
-            uint64_t qd0[2], qd1[2];
-            for (int x = 0; x < 2; ++x) {
-                qd0[x] = umma_desc_sw128(smem_u32(sm.q[x][0]), 16, 1024);
-                qd1[x] = umma_desc_sw128(smem_u32(sm.q[x][1]), 16, 1024);
-            }
-            int n_pv[2] = {0, 0};
-            mbar_wait(&sm.q_full, 0);
+            mbar_wait(&sm.q_ready, 0);
             tc_fence_after();
             for (int jj = 0; jj <= ntiles; ++jj) {
-                const int st = jj % kKvStages;
-                const int pj = jj - 1;
-                const int pst = pj % kKvStages;
                 if (jj < ntiles) {
+                    const int st = jj % kKvStages;
+                    const int sb = jj & 1;
+                    const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
+                    const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
                     mbar_wait(&sm.k_full[st], (jj / kKvStages) & 1);
                     tc_fence_after();
+                    const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
+                    const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
+                    const uint32_t dS = tmem + kColS0 + 128u * static_cast<uint32_t>(sb);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) { // K = 16 bf16 = 8 TMEM columns of Q
+                        const uint64_t bd = (kk < 4 ? kd0 : kd1) + 2 * (kk & 3);
+                        mma_bf16_ts(dS, tmem + kColQ + 8 * kk, bd, idesc_s, kk > 0);
+                    }
+                    tc_commit(&sm.s_full[sb]);
                 }
-                if (pj >= 0) {
+                if (jj > 0) {
+                    const int pj = jj - 1;
+                    const int pst = pj % kKvStages;
+                    const int psb = pj & 1;
+                    const int jp = static_cast<int>(sm.tiles[pj] & 0xFFFFu);
+                    const int steps = jp == 0 ? 2 : 8;
+                    mbar_wait(&sm.p_full[psb], (pj >> 1) & 1);
                     mbar_wait(&sm.v_full[pst], (pj / kKvStages) & 1);
                     tc_fence_after();
+                    const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
+                    const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(psb);
+                    for (int kk = 0; kk < steps; ++kk)
+                        mma_bf16_ts(tmem + kColO, aP + 8 * kk, vd + 128 * kk, // +16 keys = 2 KB
+                                    idesc_pv, (pj > 0 || kk > 0) ? 1u : 0u);
+                    tc_commit(&sm.kv_empty[pst]);
+                    tc_commit(&sm.pv_done[psb]);
                 }
-                for (int x = 0; x < 2; ++x) {
-                    // O_x += P_x(pj) V_pj — before S_x(jj) overwrites P_x
-                    if (pj >= 0 && need(pj, x)) {
-                        mbar_wait(&sm.p_full[x], n_pv[x] & 1);
-                        tc_fence_after();
-                        const int jp = static_cast<int>(sm.tiles[pj] & ((1u << kTileBits) - 1u));
-                        const int steps = jp == 0 ? 2 : 8;
-                        const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
-                        const uint32_t aP = tmem + kColS + 128u * x;
-                        for (int kk = 0; kk < steps; ++kk)
-                            mma_bf16_ts(tmem + kColO + 128u * x, aP + 8 * kk, vd + 128 * kk, // +16 keys
-                                        idesc_pv, (n_pv[x] > 0 || kk > 0) ? 1u : 0u);
-                        tc_commit(&sm.pv_done[x]);
-                        ++n_pv[x];
-                    }
-                    // S_x = Q_x K_jj
-                    if (jj < ntiles && need(jj, x)) {
-                        const int j = static_cast<int>(sm.tiles[jj] & ((1u << kTileBits) - 1u));
-                        const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
-                        const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
-                        const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            const uint64_t a = (kk < 4 ? qd0[x] : qd1[x]) + 2 * (kk & 3);
-                            const uint64_t bd = (kk < 4 ? kd0 : kd1) + 2 * (kk & 3);
-                            mma_bf16_ss(tmem + kColS + 128u * x, a, bd, idesc_s, kk > 0);
-                        }
-                        tc_commit(&sm.s_full[x]);
-                    }
-                }
-                if (pj >= 0) tc_commit(&sm.kv_empty[pst]);
             }
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ softmax
-        const int x = (warp - 4) >> 2;           // 0: tile A, 1: tile B
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
-        const int half = r >> 6;                 // head within the tile
-        const int hx = 2 * x + half;             // head within the quad
-        const int h = hbase + hx;
+        const int half = r >> 6;                 // 0: head hA, 1: head hA + 1
+        const int h = hA + half;
         const int64_t grow = q0 + (r & 63);
-        const bool row_ok = grow < tokens && hx < nh;
+        const bool row_ok = grow < tokens && (half == 0 || hasB);
         const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        const uint32_t oAddr = lane_addr + kColO + 128u * x;
-        const uint32_t sAddr = lane_addr + kColS + 128u * x;
-        SoftmaxState st;
-        int t = 0; // tiles processed by this M=128 tile
-        for (int jj = 0; jj < ntiles; ++jj) {
-            const uint32_t info = sm.tiles[jj];
-            if (((info >> (kTileBits + 8 * x)) & 0xFFu) == 0) continue; // tile-uniform
-            const int j = static_cast<int>(info & ((1u << kTileBits) - 1u));
-            const uint32_t nib = (info >> (kTileBits + 4 * hx)) & 0xFu;
-            const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
-            const int64_t lim = row_ok ? grow - key0 : -1; // valid columns c <= lim
-            mbar_wait(&sm.s_full[x], t & 1);
-            tc_fence_after();
-            if (j == 0)
-                softmax_tile<32>(sAddr, oAddr, nib, lim, scale_log2, st, &sm.pv_done[x], (t - 1) & 1);
-            else
-                softmax_tile<128>(sAddr, oAddr, nib, lim, scale_log2, st, &sm.pv_done[x], (t - 1) & 1);
+        // Q row -> TMEM columns [kColQ, kColQ + 64): the A operand of S = Q K^T
+        {
+            uint32_t a[32];
+            const uint4 *src = reinterpret_cast<const uint4 *>(
+                q + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint4 w = row_ok ? __ldg(src + 8 * hf + e) : make_uint4(0, 0, 0, 0);
+                    a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
+                }
+                tmem_st32(lane_addr + kColQ + 32 * hf, a);
+            }
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.p_full[x]);
-            ++t;
+            if (lane == 0) mbar_arrive(&sm.q_ready);
+        }
+        SoftmaxState st;
+        for (int jj = 0; jj < ntiles; ++jj) {
+            const int sb = jj & 1;
+            const uint32_t info = sm.tiles[jj];
+            const int j = static_cast<int>(info & 0xFFFFu);
+            const uint32_t nib = (info >> (16 + 4 * half)) & 0xFu;
+            const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
+            const int64_t lim = row_ok ? grow - key0 : -1; // valid columns c <= lim
+            const uint32_t sAddr = lane_addr + kColS0 + 128u * sb;
+            mbar_wait(&sm.s_full[sb], (jj >> 1) & 1);
+            tc_fence_after();
+            const int pj = jj - 1;
+            if (j == 0)
+                softmax_tile<32>(sAddr, lane_addr + kColO, nib, lim, scale_log2, st,
+                                 &sm.pv_done[pj & 1], (pj >> 1) & 1);
+            else
+                softmax_tile<128>(sAddr, lane_addr + kColO, nib, lim, scale_log2, st,
+                                  &sm.pv_done[pj & 1], (pj >> 1) & 1);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.p_full[sb]);
         }
         // ---- epilogue: O / l -> bf16
-        if (t > 0) {
-            mbar_wait(&sm.pv_done[x], (t - 1) & 1);
+        if (ntiles > 0) {
+            const int last = ntiles - 1;
+            mbar_wait(&sm.pv_done[last & 1], (last >> 1) & 1);
             tc_fence_after();
         }
         const float inv_l = st.l_run > 0.0f ? 1.0f / st.l_run : 0.0f;
@@ -437,8 +433,8 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
             uint32_t o[32];
-            if (t > 0) {
-                tmem_ld32(oAddr + 32 * cc, o);
+            if (ntiles > 0) {
+                tmem_ld32(lane_addr + kColO + 32 * cc, o);
                 tmem_ld_wait();
             } else {
 #pragma unroll
@@ -469,10 +465,10 @@ sparse_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_c
 
 size_t attention_smem_bytes() { return sizeof(AttnSmem) + 1024; }
 
-cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &tm_k,
-                                    const CUtensorMap &tm_v, const uint32_t *mask, void *out,
-                                    int32_t *coverage, int64_t batch, int64_t tokens, int hq,
-                                    int hkv, float scale_log2, cudaStream_t stream) {
+cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
+                                    const uint32_t *mask, void *out, int32_t *coverage,
+                                    int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
+                                    cudaStream_t stream) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     if (nq / 2 + 3 > kMaxTiles) return cudaErrorInvalidValue;
     static bool configured = false;
@@ -484,11 +480,11 @@ cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    const int nquads = (hq / hkv + 3) / 4;
-    const int64_t grid = batch * hkv * nquads * nq;
+    const int npairs = (hq / hkv + 1) / 2;
+    const int64_t grid = batch * hkv * npairs * nq;
     sparse_attention_kernel<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
-        tm_q, tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out), coverage, tokens, hq, hkv,
-        scale_log2);
+        static_cast<const __nv_bfloat16 *>(q), tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out),
+        coverage, tokens, hq, hkv, scale_log2);
     return cudaGetLastError();
 }
 

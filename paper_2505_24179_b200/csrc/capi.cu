@@ -277,12 +277,11 @@ int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void 
                    const sale_b200_shape &s, const uint32_t *mask, void *out, int32_t *coverage,
                    cudaStream_t stream) {
     int st;
-    CUtensorMap tq, tk, tv;
-    if ((st = make_map(ctx, &tq, q, true, s.batch, s.tokens, s.q_heads, 64, 64))) return st;
+    CUtensorMap tk, tv;
     if ((st = make_map(ctx, &tk, k, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
     if ((st = make_map(ctx, &tv, v, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
     const float scale_log2 = inv_sqrt_dim(s.head_dim) * 1.4426950408889634f;
-    SALE_CUDA(ctx, launch_sparse_attention(tq, tk, tv, mask, out, coverage, s.batch, s.tokens,
+    SALE_CUDA(ctx, launch_sparse_attention(q, tk, tv, mask, out, coverage, s.batch, s.tokens,
                                            static_cast<int>(s.q_heads), static_cast<int>(s.kv_heads),
                                            scale_log2, stream));
     mark(ctx, 5, stream);

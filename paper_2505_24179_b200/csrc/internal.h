@@ -36,10 +36,10 @@ cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, 
                             cudaStream_t stream);
 
 size_t attention_smem_bytes();
-cudaError_t launch_sparse_attention(const CUtensorMap &tm_q, const CUtensorMap &tm_k,
-                                    const CUtensorMap &tm_v, const uint32_t *mask, void *out,
-                                    int32_t *coverage, int64_t batch, int64_t tokens, int hq,
-                                    int hkv, float scale_log2, cudaStream_t stream);
+cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
+                                    const uint32_t *mask, void *out, int32_t *coverage,
+                                    int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
+                                    cudaStream_t stream);
 
 cudaError_t launch_flop_count(const uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
                               int64_t *counts, cudaStream_t stream);
