@@ -201,7 +201,9 @@ def run_b200(a):
     world, rank, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
+        # one GPU per rank; more ranks than GPUs (a functional check on a
+        # single-GPU box) share devices round-robin
+        torch.cuda.set_device(local % torch.cuda.device_count())
         dist.init_process_group("nccl")
     else:
         torch.cuda.set_device(0)

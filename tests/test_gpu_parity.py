@@ -146,6 +146,22 @@ def test_selection_llama_4k(torch):
     _check_selection(inp, 0.004)
 
 
+def test_selection_qwen_group_of_seven(torch):
+    """configs[3] shape family: Qwen2.5-7B has 28 Q / 4 KV heads (G = 7, not a
+    multiple of the estimator's 4-head CTAs or the attention's head pairs)."""
+    inp = Inputs("sink_local", 13, 1, 1536, 14, 2)
+    cells, _ = _check_selection(inp, [0.004, 0.016] * 7)
+    q, k, v = inp.torch()
+    mask = torch.from_numpy(sale.pack_mask(cells, inp.N).view(np.int32)).cuda()
+    out, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True)
+    ref = _oracle_attention(inp, cells, inp.heads())
+    out, cov = _to_np(out.float()), _to_np(cov)
+    for (b, h), (o, rcov, st) in ref.items():
+        got = out[b, :, h, :inp.d]
+        assert max_abs(got, o) < ATOL_MAX and mean_abs(got, o) < ATOL_MEAN
+        np.testing.assert_array_equal(cov[b, h], rcov)
+
+
 def test_selection_gaussian_batch(torch):
     inp = Inputs("gaussian", 3, 2, 1536, 4, 1)
     _check_selection(inp, 0.004)
