@@ -35,7 +35,7 @@
 
 namespace sale_b200 {
 
-constexpr int kAttnThreads = 256;
+constexpr int kAttnThreads = 352;  // 3 control warps + 2 softmax warpgroups (warps 3-10)
 constexpr int kMaxTiles = 4200;                // supports N <= 512K
 constexpr int kKvStages = 3;
 constexpr int kTileBytesHalf = 128 * 64 * 2;   // 128 rows x 64 bf16 = 16 KB
@@ -48,7 +48,10 @@ struct AttnSmem {
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
     int ntiles;
-    int warp_cnt[8];
+    int warp_cnt[kAttnThreads / 32];
+    float xch[2][2][128];   // [tile parity][column half][row]: partial row max
+    float fin_l[128];       // end: column-half-1 partial l and coverage
+    int fin_cov[128];
     uint32_t tiles[kMaxTiles]; // j | bits8 << 16
 };
 
@@ -85,139 +88,165 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&p);
 }
 
-struct SoftmaxState {
-    float m_run = -INFINITY; // running max, exp2 domain (logit * scale_log2)
-    float l_run = 0.0f;      // running sum of p
-    int cov = 0;             // attended tokens
-};
-
-// One S tile of one row (thread): mask, lazy online-softmax update, P -> TMEM.
-// NK = keys in the tile (32 for the sink tile, 128 otherwise). S holds raw
-// fp32 logits*sqrt(d) bits; P (bf16 pairs) is written over the first NK/2
-// columns of the same buffer.
-template <int NK>
-__device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uint32_t nib,
-                                             int64_t lim, float scale_log2, SoftmaxState &st,
-                                             uint64_t *pv_prev, uint32_t pv_parity) {
-    // The other head of the pair selected this tile, this warp's rows did not
-    // (or they are all in the causal future): P = 0, no exp work.
-    if (__all_sync(0xffffffffu, nib == 0u || lim < 0)) {
-        uint32_t z[32];
+// O (this thread's 64-column half) *= alpha, once PV of every earlier tile has
+// landed in O.
+__device__ __forceinline__ void rescale_o(uint32_t oAddr, float alpha, uint64_t *pv_prev,
+                                          uint32_t pv_parity) {
+    mbar_wait(pv_prev, pv_parity);
+    tc_fence_after();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) z[e] = 0u;
-        if constexpr (NK == 128) {
-            tmem_st32(sAddr, z);
-            tmem_st32(sAddr + 32, z);
-        } else {
-            tmem_st16(sAddr, *reinterpret_cast<uint32_t(*)[16]>(&z[0]));
-        }
-        tmem_st_wait();
-        return;
-    }
-    uint32_t s[NK];
+    for (int cc = 0; cc < 2; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(oAddr + 32 * cc, o);
+        tmem_ld_wait();
 #pragma unroll
-    for (int c4 = 0; c4 < NK / 32; ++c4)
-        tmem_ld32(sAddr + 32 * c4, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c4]));
-    tmem_ld_wait();
-    // column c valid iff its 32-key sub-block is selected and c <= lim (causal);
-    // fully selected, fully past tiles skip the per-element test.
-    const bool full = nib == ((1u << (NK / 32)) - 1u) && lim >= NK - 1;
-    int nvalid = NK;
-    if (!full) {
-        nvalid = 0;
-#pragma unroll
-        for (int c = 0; c < NK; ++c) {
-            const bool ok = ((nib >> (c >> 5)) & 1u) && c <= lim;
-            s[c] = ok ? s[c] : __float_as_uint(-INFINITY);
-            nvalid += ok ? 1 : 0;
-        }
-    }
-    float mt = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < NK; c += 2) mt = fmax3(mt, __uint_as_float(s[c]), __uint_as_float(s[c + 1]));
-    const float m_new = fmaxf(st.m_run, mt * scale_log2);
-    const bool need = st.m_run != -INFINITY && m_new > st.m_run + 8.0f;
-    if (st.m_run == -INFINITY) st.m_run = m_new;
-    if (__any_sync(0xffffffffu, need)) {
-        // O must hold PV of every earlier tile before it is rescaled
-        mbar_wait(pv_prev, pv_parity);
-        tc_fence_after();
-        const float alpha = need ? ex2_approx(st.m_run - m_new) : 1.0f;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(oAddr + 32 * cc, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(oAddr + 32 * cc, o);
-        }
-        tmem_st_wait();
-        if (need) {
-            st.l_run *= alpha;
-            st.m_run = m_new;
-        }
-    }
-    // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
-    // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
-    const float neg_m = st.m_run == -INFINITY ? 0.0f : -st.m_run;
-    const unsigned long long sc2 = pack_f2(scale_log2, scale_log2), nm2 = pack_f2(neg_m, neg_m);
-    unsigned long long psum2 = 0ull;
-    if (NK == 128 && __all_sync(0xffffffffu, full)) {
-        // Full tiles: one pair in four takes exp2 on the FMA pipe (Cody-Waite
-        // split + degree-3 polynomial, rel. err 1e-4 < bf16's 2^-8) so the
-        // MUFU pipe (16 ex2/clk/SM) stops being the co-bottleneck with the MMA.
-#pragma unroll
-        for (int c2 = 0; c2 < NK / 2; ++c2) {
-            unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
-            ffma2_f32(x, sc2, nm2);
-            float p0, p1;
-            if ((c2 & 3) == 3) {
-                const unsigned long long xc =
-                    pack_f2(fmaxf(__uint_as_float(static_cast<uint32_t>(x)), -125.0f),
-                            fmaxf(__uint_as_float(static_cast<uint32_t>(x >> 32)), -125.0f));
-                unsigned long long t = xc;
-                fadd2_f32(t, pack_f2(12582912.0f, 12582912.0f));   // round to integer
-                unsigned long long r = t;
-                fadd2_f32(r, pack_f2(-12582912.0f, -12582912.0f)); // the integer, as float
-                unsigned long long f = r ^ 0x8000000080000000ull;  // -r
-                fadd2_f32(f, xc);                                  // f = x - r in [-.5, .5]
-                unsigned long long pp = pack_f2(0.05592204f, 0.05592204f);
-                ffma2_f32(pp, f, pack_f2(0.24264008f, 0.24264008f));
-                ffma2_f32(pp, f, pack_f2(0.69312102f, 0.69312102f));
-                ffma2_f32(pp, f, pack_f2(0.99992448f, 0.99992448f));
-                p0 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp)) +
-                                    (static_cast<int>(static_cast<uint32_t>(t)) << 23));
-                p1 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp >> 32)) +
-                                    (static_cast<int>(static_cast<uint32_t>(t >> 32)) << 23));
-            } else {
-                p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
-                p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
-            }
-            fadd2_f32(psum2, pack_f2(p0, p1));
-            s[c2] = pack_bf16x2(p0, p1);
-        }
-    } else {
-#pragma unroll
-        for (int c2 = 0; c2 < NK / 2; ++c2) {
-            unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
-            ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
-            const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
-            const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
-            fadd2_f32(psum2, pack_f2(p0, p1));
-            s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
-        }
-    }
-    st.l_run += __uint_as_float(static_cast<uint32_t>(psum2)) +
-                __uint_as_float(static_cast<uint32_t>(psum2 >> 32));
-    st.cov += nvalid;
-    if constexpr (NK == 128) {
-        tmem_st32(sAddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_st32(sAddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-    } else {
-        tmem_st16(sAddr, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
+        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+        tmem_st32(oAddr + 32 * cc, o);
     }
     tmem_st_wait();
+}
+
+struct SoftmaxState {
+    float m_run = -INFINITY; // running max, exp2 domain (logit * scale_log2)
+    float l_run = 0.0f;      // running sum of p over this thread's column half
+    int cov = 0;             // attended tokens in this thread's column half
+};
+
+// One S tile, one row, one column half (thread). The two softmax warpgroups
+// split every tile's columns: warpgroup w owns tile columns [NC*w, NC*w + NC)
+// (NC = 64 for segment tiles; the 32-key sink tile is all warpgroup 0's, NC = 32,
+// and warpgroup 1 takes NC = 0). The row max is combined through shared memory
+// (xch, one named barrier per lane quadrant = the two warps that own the same
+// TMEM lanes); each half keeps its own partial l and coverage, summed at the
+// end. Both halves therefore see the same running max and take the same lazy
+// rescale decisions. S holds raw fp32 logits*sqrt(d); the bf16 P pairs of
+// columns [c0, c0+NC) are written to TMEM columns [c0/2, c0/2 + NC/2) of the
+// same buffer (written only after the barrier, i.e. after both halves have
+// read their S columns).
+template <int NC>
+__device__ __forceinline__ void softmax_part(uint32_t sAddr, uint32_t pAddr, uint32_t oAddr,
+                                             uint32_t nib, int64_t lim, float scale_log2,
+                                             SoftmaxState &st, float *xch_mine,
+                                             const float *xch_other, uint32_t bar_id,
+                                             uint64_t *pv_prev, uint32_t pv_parity) {
+    constexpr int NS = NC / 32 > 0 ? NC / 32 : 1; // 32-key sub-blocks in this half
+    // nib: this half's sub-block bits; lim: valid columns c <= lim (half-relative)
+    const bool any_valid = NC > 0 && nib != 0u && lim >= 0;
+    const bool zero = __all_sync(0xffffffffu, !any_valid);
+    uint32_t s[NC > 0 ? NC : 1];
+    float mt = -INFINITY;
+    int nvalid = 0;
+    bool full = false;
+    if constexpr (NC > 0) {
+        if (!zero) {
+#pragma unroll
+            for (int c4 = 0; c4 < NC / 32; ++c4)
+                tmem_ld32(sAddr + 32 * c4, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c4]));
+            tmem_ld_wait();
+            full = nib == ((1u << NS) - 1u) && lim >= NC - 1;
+            nvalid = NC;
+            if (!full) {
+                nvalid = 0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const bool ok = ((nib >> (c >> 5)) & 1u) && c <= lim;
+                    s[c] = ok ? s[c] : __float_as_uint(-INFINITY);
+                    nvalid += ok ? 1 : 0;
+                }
+            }
+            // four independent max chains (latency), then combined
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int c = 0; c < NC; c += 8)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    mx[u] = fmax3(mx[u], __uint_as_float(s[c + 2 * u]), __uint_as_float(s[c + 2 * u + 1]));
+            mt = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
+        }
+    }
+    // combine the row max with the other column half
+    *xch_mine = mt;
+    named_bar_sync(bar_id, 64);
+    mt = fmaxf(mt, *xch_other);
+    const float m_new = fmaxf(st.m_run, mt * scale_log2);
+    // lazy rescale: only when the running max grows by > 8 (exp2 domain); P is
+    // computed against the new max, O and l are rescaled after P is stored
+    // (fewer live registers), before p_full releases PV of this tile.
+    const bool need = st.m_run != -INFINITY && m_new > st.m_run + 8.0f;
+    const float alpha = need ? ex2_approx(st.m_run - m_new) : 1.0f;
+    if (st.m_run == -INFINITY || need) st.m_run = m_new;
+    if (need) st.l_run *= alpha;
+    const bool any_need = __any_sync(0xffffffffu, need);
+    if constexpr (NC > 0) {
+        if (zero) {
+            // nothing of this half is attended by the warp's rows: P = 0, no exp work
+            uint32_t z[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) z[e] = 0u;
+            if constexpr (NC == 64) tmem_st32(pAddr, z);
+            else tmem_st16(pAddr, *reinterpret_cast<uint32_t(*)[16]>(&z[0]));
+            tmem_st_wait();
+            if (any_need) rescale_o(oAddr, alpha, pv_prev, pv_parity);
+            return;
+        }
+        // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
+        // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
+        const float neg_m = st.m_run == -INFINITY ? 0.0f : -st.m_run;
+        const unsigned long long sc2 = pack_f2(scale_log2, scale_log2), nm2 = pack_f2(neg_m, neg_m);
+        unsigned long long psum2 = 0ull;
+        if (NC == 64 && __all_sync(0xffffffffu, full)) {
+            // Full halves: one pair in four takes exp2 on the FMA pipe (Cody-Waite
+            // split + degree-3 polynomial, rel. err 1e-4 < bf16's 2^-8) so the
+            // MUFU pipe (16 ex2/clk/SM) stops being the co-bottleneck with the MMA.
+#pragma unroll
+            for (int c2 = 0; c2 < NC / 2; ++c2) {
+                unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
+                ffma2_f32(x, sc2, nm2);
+                float p0, p1;
+                if ((c2 & 3) == 3) {
+                    const unsigned long long xc =
+                        pack_f2(fmaxf(__uint_as_float(static_cast<uint32_t>(x)), -125.0f),
+                                fmaxf(__uint_as_float(static_cast<uint32_t>(x >> 32)), -125.0f));
+                    unsigned long long t = xc;
+                    fadd2_f32(t, pack_f2(12582912.0f, 12582912.0f));   // round to integer
+                    unsigned long long r = t;
+                    fadd2_f32(r, pack_f2(-12582912.0f, -12582912.0f)); // the integer, as float
+                    unsigned long long f = r ^ 0x8000000080000000ull;  // -r
+                    fadd2_f32(f, xc);                                  // f = x - r in [-.5, .5]
+                    unsigned long long pp = pack_f2(0.05592204f, 0.05592204f);
+                    ffma2_f32(pp, f, pack_f2(0.24264008f, 0.24264008f));
+                    ffma2_f32(pp, f, pack_f2(0.69312102f, 0.69312102f));
+                    ffma2_f32(pp, f, pack_f2(0.99992448f, 0.99992448f));
+                    p0 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp)) +
+                                        (static_cast<int>(static_cast<uint32_t>(t)) << 23));
+                    p1 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp >> 32)) +
+                                        (static_cast<int>(static_cast<uint32_t>(t >> 32)) << 23));
+                } else {
+                    p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
+                    p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
+                }
+                fadd2_f32(psum2, pack_f2(p0, p1));
+                s[c2] = pack_bf16x2(p0, p1);
+            }
+        } else {
+#pragma unroll
+            for (int c2 = 0; c2 < NC / 2; ++c2) {
+                unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
+                ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
+                const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
+                const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
+                fadd2_f32(psum2, pack_f2(p0, p1));
+                s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
+            }
+        }
+        st.l_run += __uint_as_float(static_cast<uint32_t>(psum2)) +
+                    __uint_as_float(static_cast<uint32_t>(psum2 >> 32));
+        st.cov += nvalid;
+        if constexpr (NC == 64) tmem_st32(pAddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        else tmem_st16(pAddr, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
+        tmem_st_wait();
+    }
+    if (any_need) rescale_o(oAddr, alpha, pv_prev, pv_parity);
 }
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -226,8 +255,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                         __nv_bfloat16 *__restrict__ out, int32_t *__restrict__ coverage,
                         int64_t tokens, int hq, int hkv, float scale_log2) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    AttnSmem &sm = *reinterpret_cast<AttnSmem *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    AttnSmem &sm = *reinterpret_cast<AttnSmem *>(smem_raw + smem_pad_1k(smem_raw));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int tid = threadIdx.x;
@@ -252,7 +280,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
     const int64_t qend = q0 + kBlockQ < tokens ? q0 + kBlockQ : tokens;
 
     if (tid == 0) {
-        mbar_init(&sm.q_ready, 4);
+        mbar_init(&sm.q_ready, 8);
         for (int s = 0; s < kKvStages; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.v_full[s], 1);
@@ -260,7 +288,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.s_full[s], 1);
-            mbar_init(&sm.p_full[s], 4);
+            mbar_init(&sm.p_full[s], 8);
             mbar_init(&sm.pv_done[s], 1);
         }
         sm.ntiles = 0;
@@ -372,69 +400,87 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                 }
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp >= 3) {
         // ------------------------------------------------------------ softmax
-        const int quad = warp & 3;
+        const int wg = (warp - 3) >> 2;          // column half of every tile
+        const int quad = warp & 3;               // TMEM lane quadrant (warp id % 4)
         const int r = quad * 32 + lane;
         const int half = r >> 6;                 // 0: head hA, 1: head hA + 1
         const int h = hA + half;
         const int64_t grow = q0 + (r & 63);
         const bool row_ok = grow < tokens && (half == 0 || hasB);
         const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        // Q row -> TMEM columns [kColQ, kColQ + 64): the A operand of S = Q K^T
+        const uint32_t bar_id = 1 + quad;
+        // Q row half -> TMEM columns [kColQ + 32 wg, +32): the A operand of S = Q K^T
         {
             uint32_t a[32];
             const uint4 *src = reinterpret_cast<const uint4 *>(
-                q + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim);
+                q + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim + 64 * wg);
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint4 w = row_ok ? __ldg(src + 8 * hf + e) : make_uint4(0, 0, 0, 0);
-                    a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
-                }
-                tmem_st32(lane_addr + kColQ + 32 * hf, a);
+            for (int e = 0; e < 8; ++e) {
+                const uint4 w = row_ok ? __ldg(src + e) : make_uint4(0, 0, 0, 0);
+                a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
             }
+            tmem_st32(lane_addr + kColQ + 32 * wg, a);
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.q_ready);
         }
         SoftmaxState st;
+        const uint32_t oAddr = lane_addr + kColO + 64u * wg;
         for (int jj = 0; jj < ntiles; ++jj) {
             const int sb = jj & 1;
             const uint32_t info = sm.tiles[jj];
             const int j = static_cast<int>(info & 0xFFFFu);
             const uint32_t nib = (info >> (16 + 4 * half)) & 0xFu;
             const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
-            const int64_t lim = row_ok ? grow - key0 : -1; // valid columns c <= lim
-            const uint32_t sAddr = lane_addr + kColS0 + 128u * sb;
+            const uint32_t sBase = lane_addr + kColS0 + 128u * sb;
+            float *xm = &sm.xch[sb][wg][r];
+            const float *xo = &sm.xch[sb][wg ^ 1][r];
             mbar_wait(&sm.s_full[sb], (jj >> 1) & 1);
             tc_fence_after();
             const int pj = jj - 1;
-            if (j == 0)
-                softmax_tile<32>(sAddr, lane_addr + kColO, nib, lim, scale_log2, st,
-                                 &sm.pv_done[pj & 1], (pj >> 1) & 1);
-            else
-                softmax_tile<128>(sAddr, lane_addr + kColO, nib, lim, scale_log2, st,
-                                  &sm.pv_done[pj & 1], (pj >> 1) & 1);
+            // The 32-key sink tile runs through the same 64-column code: its
+            // columns >= 32 (stale S data) are masked like unselected sub-blocks,
+            // so warpgroup 1 always takes the zero path there.
+            const uint32_t nib_half = j == 0 ? (wg == 0 ? (nib & 1u) : 0u) : (nib >> (2 * wg)) & 3u;
+            const int64_t lim = row_ok ? grow - key0 - 64 * wg : -1;
+            softmax_part<64>(sBase + 64u * wg, sBase + 32u * wg, oAddr, nib_half, lim, scale_log2, st,
+                             xm, xo, bar_id, &sm.pv_done[pj & 1], (pj >> 1) & 1);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.p_full[sb]);
         }
-        // ---- epilogue: O / l -> bf16
+        // ---- epilogue: l = l_half0 + l_half1, O / l -> bf16 (each half its 64 columns)
+        if (wg == 1) {
+            sm.fin_l[r] = st.l_run;
+            sm.fin_cov[r] = st.cov;
+        }
+        named_bar_sync(bar_id, 64);
+        float l_tot = st.l_run;
+        int cov_tot = st.cov;
+        if (wg == 0) {
+            l_tot += sm.fin_l[r];
+            cov_tot += sm.fin_cov[r];
+        }
+        named_bar_sync(bar_id, 64);
+        if (wg == 0) sm.fin_l[r] = l_tot; // one sum, used by both halves
+        named_bar_sync(bar_id, 64);
+        if (wg == 1) l_tot = sm.fin_l[r];
         if (ntiles > 0) {
             const int last = ntiles - 1;
             mbar_wait(&sm.pv_done[last & 1], (last >> 1) & 1);
             tc_fence_after();
         }
-        const float inv_l = st.l_run > 0.0f ? 1.0f / st.l_run : 0.0f;
-        __nv_bfloat16 *dst = out + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim;
+        const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
+        __nv_bfloat16 *dst =
+            out + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim + 64 * wg;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
+        for (int cc = 0; cc < 2; ++cc) {
             uint32_t o[32];
             if (ntiles > 0) {
-                tmem_ld32(lane_addr + kColO + 32 * cc, o);
+                tmem_ld32(oAddr + 32 * cc, o);
                 tmem_ld_wait();
             } else {
 #pragma unroll
@@ -451,7 +497,8 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                 for (int e = 0; e < 4; ++e) d4[e] = w[e];
             }
         }
-        if (row_ok && coverage) coverage[(static_cast<int64_t>(b) * hq + h) * tokens + grow] = st.cov;
+        if (wg == 0 && row_ok && coverage)
+            coverage[(static_cast<int64_t>(b) * hq + h) * tokens + grow] = cov_tot;
     }
     tc_fence_before();
     __syncthreads();

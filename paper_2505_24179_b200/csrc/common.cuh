@@ -24,6 +24,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Bytes to add to the dynamic shared memory base to reach 1 KB alignment
+// (SW128 tiles). Indexing smem_raw with it keeps the compiler's knowledge that
+// the struct lives in shared memory (LDS/STS, not generic LD/ST), which a
+// round trip through uintptr_t would lose.
+__device__ __forceinline__ uint32_t smem_pad_1k(const void *base) {
+    return (1024u - (smem_u32(base) & 1023u)) & 1023u;
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ bool elect_one() {

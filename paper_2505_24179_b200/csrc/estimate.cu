@@ -70,8 +70,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 float inv_sqrt_d, int32_t *__restrict__ dbg_max) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // dynamic smem base is only 16-B aligned by contract: round up to 1 KB
-    EstSmem &sm = *reinterpret_cast<EstSmem *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    EstSmem &sm = *reinterpret_cast<EstSmem *>(smem_raw + smem_pad_1k(smem_raw));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
