@@ -163,6 +163,12 @@ int sale_b200_set_timing(sale_b200_ctx *ctx, int enable);
  * enable != 0 turns collection on for later launches. counters may be NULL
  * (then it must hold 16 entries otherwise). */
 int sale_b200_estimator_profile(sale_b200_ctx *ctx, int enable, uint64_t *counters);
+
+/* Diagnostics: cycle counters of the attention kernel (16 entries): softmax
+ * loop, S-ready waits, softmax compute, tiles (one softmax warp, summed over
+ * CTAs); MMA loop, K / P / V waits, CTAs; [10] epilogue. Reads and resets;
+ * enable != 0 turns collection on for later launches. */
+int sale_b200_attention_profile(sale_b200_ctx *ctx, int enable, uint64_t *counters);
 int sale_b200_stage_times(sale_b200_ctx *ctx, float *ms);
 
 /* ---- synthetic workload (host, not the hot path) --------------------------

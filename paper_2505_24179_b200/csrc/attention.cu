@@ -55,6 +55,14 @@ struct AttnSmem {
     uint32_t tiles[kMaxTiles]; // j | bits8 << 16
 };
 
+// Optional cycle instrumentation (sale_b200_attention_profile): [0] softmax
+// loop total, [1] S-ready waits, [2] softmax_part time, [3] tiles (warp 3,
+// lane 0, summed over CTAs); [4] MMA loop total, [5] K waits, [6] P waits,
+// [7] V waits, [8] CTAs, [9] prologue (start -> tile list ready, thread 0),
+// [10] epilogue (last tile -> end, warp 3 lane 0).
+__device__ int g_attn_prof_on = 0;
+__device__ unsigned long long g_attn_prof[16];
+
 namespace {
 
 __device__ __forceinline__ uint32_t mask_bits4(const uint32_t *row, int64_t words, int64_t j0) {
@@ -81,6 +89,17 @@ __device__ __forceinline__ void ffma2_f32(unsigned long long &x, unsigned long l
 }
 __device__ __forceinline__ void fadd2_f32(unsigned long long &x, unsigned long long a) {
     asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(a));
+}
+
+__device__ __forceinline__ void fsub2_f32(unsigned long long &x, unsigned long long a) {
+    asm("sub.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(a));
+}
+// (t << 23) + p on the ALU pipe (SHF + IADD3) instead of an FMA-pipe IMAD
+__device__ __forceinline__ uint32_t shl23_add(uint32_t t, uint32_t p) {
+    uint32_t sh, r;
+    asm("shf.l.wrap.b32 %0, %1, %2, 23;" : "=r"(sh) : "r"(0u), "r"(t)); // upper word of (t:0) << 23
+    asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(sh), "r"(p));
+    return r;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -195,15 +214,16 @@ __device__ __forceinline__ void softmax_part(uint32_t sAddr, uint32_t pAddr, uin
         const unsigned long long sc2 = pack_f2(scale_log2, scale_log2), nm2 = pack_f2(neg_m, neg_m);
         unsigned long long psum2 = 0ull;
         if (NC == 64 && __all_sync(0xffffffffu, full)) {
-            // Full halves: one pair in four takes exp2 on the FMA pipe (Cody-Waite
-            // split + degree-3 polynomial, rel. err 1e-4 < bf16's 2^-8) so the
-            // MUFU pipe (16 ex2/clk/SM) stops being the co-bottleneck with the MMA.
+            // Full halves: every second pair takes exp2 on the FMA/ALU pipes
+            // (Cody-Waite split + degree-3 polynomial, rel. err 1e-4 < bf16's
+            // 2^-8), the rest on MUFU (16 ex2/clk/SM): per SMSP and tile the XU,
+            // FMA and ALU pipes then carry about equal work.
 #pragma unroll
             for (int c2 = 0; c2 < NC / 2; ++c2) {
                 unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
                 ffma2_f32(x, sc2, nm2);
                 float p0, p1;
-                if ((c2 & 3) == 3) {
+                if (c2 & 1) {
                     const unsigned long long xc =
                         pack_f2(fmaxf(__uint_as_float(static_cast<uint32_t>(x)), -125.0f),
                                 fmaxf(__uint_as_float(static_cast<uint32_t>(x >> 32)), -125.0f));
@@ -211,16 +231,16 @@ __device__ __forceinline__ void softmax_part(uint32_t sAddr, uint32_t pAddr, uin
                     fadd2_f32(t, pack_f2(12582912.0f, 12582912.0f));   // round to integer
                     unsigned long long r = t;
                     fadd2_f32(r, pack_f2(-12582912.0f, -12582912.0f)); // the integer, as float
-                    unsigned long long f = r ^ 0x8000000080000000ull;  // -r
-                    fadd2_f32(f, xc);                                  // f = x - r in [-.5, .5]
+                    unsigned long long f = xc;
+                    fsub2_f32(f, r);                                   // f = x - r in [-.5, .5]
                     unsigned long long pp = pack_f2(0.05592204f, 0.05592204f);
                     ffma2_f32(pp, f, pack_f2(0.24264008f, 0.24264008f));
                     ffma2_f32(pp, f, pack_f2(0.69312102f, 0.69312102f));
                     ffma2_f32(pp, f, pack_f2(0.99992448f, 0.99992448f));
-                    p0 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp)) +
-                                        (static_cast<int>(static_cast<uint32_t>(t)) << 23));
-                    p1 = __int_as_float(static_cast<int>(static_cast<uint32_t>(pp >> 32)) +
-                                        (static_cast<int>(static_cast<uint32_t>(t >> 32)) << 23));
+                    // 2^r * poly: integer r into the exponent field (ALU shift + add)
+                    p0 = __uint_as_float(shl23_add(static_cast<uint32_t>(t), static_cast<uint32_t>(pp)));
+                    p1 = __uint_as_float(shl23_add(static_cast<uint32_t>(t >> 32),
+                                                   static_cast<uint32_t>(pp >> 32)));
                 } else {
                     p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
                     p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
@@ -361,6 +381,9 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         // ---------------------------------------------------------------- MMA
         if (elect_one() && ntiles > 0) {
             constexpr uint32_t idesc_pv = idesc_bf16(128, 128, true);
+            const bool prof = g_attn_prof_on != 0;
+            const long long t_start = clock64();
+            long long w_k = 0, w_p = 0, w_v = 0, t0 = 0;
             mbar_wait(&sm.q_ready, 0);
             tc_fence_after();
             for (int jj = 0; jj <= ntiles; ++jj) {
@@ -369,7 +392,9 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                     const int sb = jj & 1;
                     const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
                     const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
+                    if (prof) t0 = clock64();
                     mbar_wait(&sm.k_full[st], (jj / kKvStages) & 1);
+                    if (prof) w_k += clock64() - t0;
                     tc_fence_after();
                     const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
                     const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
@@ -387,8 +412,11 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                     const int psb = pj & 1;
                     const int jp = static_cast<int>(sm.tiles[pj] & 0xFFFFu);
                     const int steps = jp == 0 ? 2 : 8;
+                    if (prof) t0 = clock64();
                     mbar_wait(&sm.p_full[psb], (pj >> 1) & 1);
+                    if (prof) { w_p += clock64() - t0; t0 = clock64(); }
                     mbar_wait(&sm.v_full[pst], (pj / kKvStages) & 1);
+                    if (prof) w_v += clock64() - t0;
                     tc_fence_after();
                     const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
                     const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(psb);
@@ -398,6 +426,13 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                     tc_commit(&sm.kv_empty[pst]);
                     tc_commit(&sm.pv_done[psb]);
                 }
+            }
+            if (prof) {
+                atomicAdd(&g_attn_prof[4], static_cast<unsigned long long>(clock64() - t_start));
+                atomicAdd(&g_attn_prof[5], static_cast<unsigned long long>(w_k));
+                atomicAdd(&g_attn_prof[6], static_cast<unsigned long long>(w_p));
+                atomicAdd(&g_attn_prof[7], static_cast<unsigned long long>(w_v));
+                atomicAdd(&g_attn_prof[8], 1ull);
             }
         }
     } else if (warp >= 3) {
@@ -429,6 +464,9 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         }
         SoftmaxState st;
         const uint32_t oAddr = lane_addr + kColO + 64u * wg;
+        const bool prof = warp == 3 && lane == 0 && g_attn_prof_on != 0;
+        const long long t_loop = clock64();
+        long long w_s = 0, t_part = 0, t1 = 0;
         for (int jj = 0; jj < ntiles; ++jj) {
             const int sb = jj & 1;
             const uint32_t info = sm.tiles[jj];
@@ -438,7 +476,9 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             const uint32_t sBase = lane_addr + kColS0 + 128u * sb;
             float *xm = &sm.xch[sb][wg][r];
             const float *xo = &sm.xch[sb][wg ^ 1][r];
+            if (prof) t1 = clock64();
             mbar_wait(&sm.s_full[sb], (jj >> 1) & 1);
+            if (prof) { const long long t2 = clock64(); w_s += t2 - t1; t1 = t2; }
             tc_fence_after();
             const int pj = jj - 1;
             // The 32-key sink tile runs through the same 64-column code: its
@@ -448,9 +488,17 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             const int64_t lim = row_ok ? grow - key0 - 64 * wg : -1;
             softmax_part<64>(sBase + 64u * wg, sBase + 32u * wg, oAddr, nib_half, lim, scale_log2, st,
                              xm, xo, bar_id, &sm.pv_done[pj & 1], (pj >> 1) & 1);
+            if (prof) t_part += clock64() - t1;
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.p_full[sb]);
+        }
+        const long long t_epi = clock64();
+        if (prof) {
+            atomicAdd(&g_attn_prof[0], static_cast<unsigned long long>(t_epi - t_loop));
+            atomicAdd(&g_attn_prof[1], static_cast<unsigned long long>(w_s));
+            atomicAdd(&g_attn_prof[2], static_cast<unsigned long long>(t_part));
+            atomicAdd(&g_attn_prof[3], static_cast<unsigned long long>(ntiles));
         }
         // ---- epilogue: l = l_half0 + l_half1, O / l -> bf16 (each half its 64 columns)
         if (wg == 1) {
@@ -499,6 +547,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         }
         if (wg == 0 && row_ok && coverage)
             coverage[(static_cast<int64_t>(b) * hq + h) * tokens + grow] = cov_tot;
+        if (prof) atomicAdd(&g_attn_prof[10], static_cast<unsigned long long>(clock64() - t_epi));
     }
     tc_fence_before();
     __syncthreads();
@@ -509,6 +558,17 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
 }
 
 } // namespace
+
+cudaError_t attention_profile(int enable, unsigned long long *out16) {
+    if (out16) {
+        cudaError_t e = cudaMemcpyFromSymbol(out16, g_attn_prof, sizeof(g_attn_prof));
+        if (e != cudaSuccess) return e;
+    }
+    unsigned long long zero[16] = {};
+    cudaError_t e = cudaMemcpyToSymbol(g_attn_prof, zero, sizeof(zero));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(g_attn_prof_on, &enable, sizeof(int));
+}
 
 size_t attention_smem_bytes() { return sizeof(AttnSmem) + 1024; }
 

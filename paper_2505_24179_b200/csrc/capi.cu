@@ -374,6 +374,13 @@ int sale_b200_estimator_profile(sale_b200_ctx *ctx, int enable, uint64_t *counte
     return SALE_B200_OK;
 }
 
+int sale_b200_attention_profile(sale_b200_ctx *ctx, int enable, uint64_t *counters) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    SALE_CUDA(ctx, cudaDeviceSynchronize());
+    SALE_CUDA(ctx, attention_profile(enable, reinterpret_cast<unsigned long long *>(counters)));
+    return SALE_B200_OK;
+}
+
 int sale_b200_set_timing(sale_b200_ctx *ctx, int enable) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);

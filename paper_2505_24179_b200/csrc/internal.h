@@ -36,6 +36,7 @@ cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, 
                             cudaStream_t stream);
 
 size_t attention_smem_bytes();
+cudaError_t attention_profile(int enable, unsigned long long *out16);
 cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
                                     const uint32_t *mask, void *out, int32_t *coverage,
                                     int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
