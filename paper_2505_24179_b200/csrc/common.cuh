@@ -74,6 +74,32 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// Spin on mbarrier.test_wait (non-blocking) instead of try_wait: reacts to the
+// phase flip without try_wait's suspend/wake-up latency; for short, hot
+// hand-offs where the waiting warp has nothing else to do.
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
+    while (!mbar_test_wait(a, parity)) {
+        if ((++spins & 4095u) == 0) {
+            if (t0 == 0) t0 = global_timer_ns();
+            else if (global_timer_ns() - t0 > 4000000000ull) __trap();
+        }
+    }
+}
+
 // Waits for the phase with the given parity. A wait that exceeds ~4 s traps
 // (turns a protocol bug into a launch error instead of a hung GPU).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
@@ -216,6 +242,26 @@ __device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-uniform issue: the whole warp executes the call (so descriptors and
+// loop state stay in uniform registers) and elect.sync picks the one lane that
+// issues. elect.sync with a full mask always picks the same lane, so a later
+// tc_commit_elect tracks exactly these MMAs.
+__device__ __forceinline__ void mma_i8_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n .reg .b32 r;\n setp.ne.b32 p, %4, 0;\n"
+        " elect.sync r|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n .reg .pred e;\n .reg .b32 r;\n elect.sync r|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
 // D[tmem] (+)= A[smem] * B[smem], bf16 x bf16 -> f32
 __device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {
@@ -276,6 +322,14 @@ __device__ __forceinline__ void tmem_ld32_pack16(uint32_t taddr, uint32_t (&r)[1
         "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"
         "%11,%12,%13,%14,%15}, [%16];"
         : SALE_R16(r, 0)
+        : "r"(taddr));
+}
+// 32 lanes x 64 columns, low 16 bits of each column packed in pairs -> 32 regs.
+__device__ __forceinline__ void tmem_ld64_pack16(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : SALE_R16(r, 0), SALE_R16(r, 16)
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {

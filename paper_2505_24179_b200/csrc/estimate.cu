@@ -143,12 +143,14 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 mbar_wait(&sm.full[st], (k / kEstStages) & 1);
                 if (prof) w_full += clock64() - t0;
                 const uint64_t bdesc = umma_desc_sw128(smem_u32(sm.bst[st]), 16, 1024);
-                for (int hh = 0; hh < nh; ++hh) {
+#pragma unroll
+                for (int hh = 0; hh < kEstHeads; ++hh) {
+                    if (hh >= nh) break;
                     // head hh owns TMEM columns [128 hh, 128 hh + 128): its
-                    // epilogue of stage k-1 had three other heads' MMAs to finish
-                    t0 = prof ? clock64() : 0;
+                    // epilogue of stage k-1 had three other heads' MMAs to finish.
+                    // (The issue latency of this thread is on the critical path:
+                    // the tensor pipe queues only a few MMAs, so nothing else here.)
                     mbar_wait(&sm.tmem_empty[hh], (k & 1) ^ 1);
-                    if (prof) w_empty += clock64() - t0;
                     tc_fence_after();
                     const uint32_t d = tmem + 128 * hh;
 #pragma unroll
@@ -211,55 +213,43 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             const uint32_t kbit = 1u << (k & 31);
             const uint32_t kb0 = (k >> 5) == 0 ? kbit : 0u, kb1 = kbit ^ kb0;
             static_assert(kSegWords == 2, "flag words");
-            // two heads per step: one tcgen05.wait::ld, two independent reductions
+            // one head at a time: its buffer is released as soon as the values
+            // are in registers (the issuer then has the other three heads' MMAs
+            // of slack), the reduction runs while the next head's MMAs execute
 #pragma unroll
-            for (int hp = 0; hp < kEstHeads; hp += 2) {
-                if (hp >= nh) break; // warp-uniform
-                const bool two = hp + 1 < nh;
+            for (int hh = 0; hh < kEstHeads; ++hh) {
+                if (hh >= nh) break; // warp-uniform
                 const long long t0 = prof ? clock64() : 0;
-                mbar_wait(&sm.tmem_full[hp], k & 1);
-                if (two) mbar_wait(&sm.tmem_full[hp + 1], k & 1);
+                mbar_wait(&sm.tmem_full[hh], k & 1);
                 if (prof) w_epi += clock64() - t0;
                 tc_fence_after();
                 if (epi_skip) { // diagnostic (profile mode 2): MMA side alone
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&sm.tmem_empty[hp]);
-                        if (two) mbar_arrive(&sm.tmem_empty[hp + 1]);
-                    }
+                    if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]);
                     continue;
                 }
-                uint32_t v[2][16];
-                tmem_ld32_pack16(acc + 128 * hp, v[0]);
-                if (two) tmem_ld32_pack16(acc + 128 * (hp + 1), v[1]);
+                uint32_t v[16];
+                tmem_ld32_pack16(acc + 128 * hh, v);
                 tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) { // registers hold the data now: release the buffers
-                    mbar_arrive(&sm.tmem_empty[hp]);
-                    if (two) mbar_arrive(&sm.tmem_empty[hp + 1]);
-                }
+                if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]); // registers hold the data now
 #pragma unroll
-                for (int x = 0; x < 2; ++x) {
-                    if (x == 1 && !two) break;
-                    const int hh = hp + x;
+                for (int s = 8; s > 0; s >>= 1)
 #pragma unroll
-                    for (int s = 8; s > 0; s >>= 1)
-#pragma unroll
-                        for (int e = 0; e < s; ++e) v[x][e] = __vmaxs2(v[x][e], v[x][e + s]);
-                    const int lo = static_cast<int16_t>(v[x][0] & 0xFFFFu);
-                    const int hi = static_cast<int16_t>(v[x][0] >> 16);
-                    const int mx = lo > hi ? lo : hi;
-                    const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
-                    const float est = __fmul_rn(rs, static_cast<float>(mx));
-                    const bool pass = est >= fb[hh];
-                    flags[hh][0] |= pass ? kb0 : 0u;
-                    flags[hh][1] |= pass ? kb1 : 0u;
-                    if (dbg)
-                        dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                                jb_base + 4 * k + chunk] = mx;
-                }
+                    for (int e = 0; e < s; ++e) v[e] = __vmaxs2(v[e], v[e + s]);
+                const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
+                const int hi = static_cast<int16_t>(v[0] >> 16);
+                const int mx = lo > hi ? lo : hi;
+                const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
+                const float est = __fmul_rn(rs, static_cast<float>(mx));
+                const bool pass = est >= fb[hh];
+                flags[hh][0] |= pass ? kb0 : 0u;
+                flags[hh][1] |= pass ? kb1 : 0u;
+                if (dbg)
+                    dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                            jb_base + 4 * k + chunk] = mx;
             }
         }
         // OR over the warp's 32 rows; the two query blocks of the tile are the
