@@ -56,6 +56,24 @@ __device__ __forceinline__ void ffma2(unsigned long long &acc, unsigned long lon
                                       unsigned long long b) {
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
 }
+// bf16 (low / high half of a 32-bit word) -> fp32 bits with a byte permute:
+// ALU pipe, where a shift would compile to an FMA-pipe IMAD that competes with
+// the dot products' FFMA2s.
+__device__ __forceinline__ uint32_t bf16lo_f32(uint32_t w) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(r) : "r"(w));
+    return r;
+}
+__device__ __forceinline__ uint32_t bf16hi_f32(uint32_t w) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0x3244;" : "=r"(r) : "r"(w));
+    return r;
+}
+__device__ __forceinline__ unsigned long long pack2u(uint32_t lo, uint32_t hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+    return r;
+}
 __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
     return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
 }
@@ -108,25 +126,38 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         sm.blk_len[tid] = len;
     }
 
-    // ---- stage Q rows and I_SL keys (bf16) with cp.async, zero-filling
-    //      rows past the sequence end.
-    constexpr int kCh = kHeadDim / 8; // 16-byte chunks per row
-    for (int idx = tid; idx < kRows * kCh; idx += kThreads) {
-        const int r = idx / kCh, ch = idx % kCh;
-        const bool ok = r < qrows;
-        const __nv_bfloat16 *src = q + ((b * tokens + q0 + (ok ? r : 0)) * hq + h) * kHeadDim + 8 * ch;
-        cp_async16(&sm.u.in.q[r][8 * ch], src, ok);
-    }
-    for (int idx = tid; idx < kMaxKeys * kCh; idx += kThreads) {
-        const int t = idx / kCh, ch = idx % kCh;
+    // ---- stage Q rows and I_SL keys (bf16) with cp.async, zero-filling rows
+    //      past the sequence end, in four channel quarters (one commit group
+    //      each): the dot chains run over c = 0..127 in order, so quarter qq's
+    //      FMAs start as soon as it has landed while the later quarters stream.
+    constexpr int kQCh = kHeadDim / 8 / 4; // 16-byte chunks per row and channel quarter
+    static_assert(kRows * kQCh == kThreads, "one Q chunk per thread and quarter");
+    // thread -> (Q row tid/4, chunk tid%4 of each quarter) and keys
+    // t = tid/4 + 64 n (n < 4, t < 224), same chunk: row offsets computed once
+    const int cq = tid & 3;
+    const int rq = tid >> 2;
+    const bool q_ok = rq < qrows;
+    const __nv_bfloat16 *q_src = q + ((b * tokens + q0 + (q_ok ? rq : 0)) * hq + h) * kHeadDim + 8 * cq;
+    const __nv_bfloat16 *k_src[4];
+    bool k_ok[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+        const int t = rq + 64 * n;
         const int slot = t / kBlockK;
-        const int64_t tok = slot < nsl ? slot_token(slot) + t % kBlockK : tokens;
-        const bool ok = tok < tokens;
-        const __nv_bfloat16 *src = k + ((b * tokens + (ok ? tok : 0)) * hkv + g) * kHeadDim + 8 * ch;
-        cp_async16(&sm.u.in.k[t][8 * ch], src, ok);
+        const int64_t tok = (t < kMaxKeys && slot < nsl) ? slot_token(slot) + t % kBlockK : tokens;
+        k_ok[n] = tok < tokens;
+        k_src[n] = k + ((b * tokens + (k_ok[n] ? tok : 0)) * hkv + g) * kHeadDim + 8 * cq;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+        cp_async16(&sm.u.in.q[rq][8 * (qq * kQCh + cq)], q_src + 32 * qq, q_ok);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            const int t = rq + 64 * n;
+            if (t < kMaxKeys) cp_async16(&sm.u.in.k[t][8 * (qq * kQCh + cq)], k_src[n] + 32 * qq, k_ok[n]);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     SALE_PHASE(1)
 
     // ---- fp32 logits: thread = 4 rows x 14 keys (kg + 16 j), sequential over c;
@@ -143,29 +174,38 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         for (int a = 0; a < 4; ++a) qw[a] = reinterpret_cast<const uint32_t *>(sm.u.in.q[rg * 4 + a]);
         const uint32_t *kw = reinterpret_cast<const uint32_t *>(sm.u.in.k[kg]);
         constexpr int kRowWords = kPitch / 2;
+#pragma unroll 1
+        for (int qq = 0; qq < 4; ++qq) {
+            // quarter qq landed (this thread's copies), then everyone's
+            if (qq == 0) asm volatile("cp.async.wait_group 3;" ::: "memory");
+            else if (qq == 1) asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else if (qq == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
 #pragma unroll 2
-        for (int cw = 0; cw < kHeadDim / 2; ++cw) {
-            uint32_t qv[4], kv[14];
+            for (int cw = 16 * qq; cw < 16 * qq + 16; ++cw) {
+                uint32_t qv[4], kv[14];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) qv[a] = qw[a][cw];
+                for (int a = 0; a < 4; ++a) qv[a] = qw[a][cw];
 #pragma unroll
-            for (int j = 0; j < 14; ++j) kv[j] = kw[(16 * j) * kRowWords + cw];
-            // c = 2cw (low halves), then c = 2cw + 1 (high halves)
+                for (int j = 0; j < 14; ++j) kv[j] = kw[(16 * j) * kRowWords + cw];
+                // c = 2cw (low halves), then c = 2cw + 1 (high halves)
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                unsigned long long kp[7];
+                for (int half = 0; half < 2; ++half) {
+                    unsigned long long kp[7];
 #pragma unroll
-                for (int p = 0; p < 7; ++p) {
-                    const uint32_t x0 = half ? (kv[2 * p] & 0xFFFF0000u) : (kv[2 * p] << 16);
-                    const uint32_t x1 = half ? (kv[2 * p + 1] & 0xFFFF0000u) : (kv[2 * p + 1] << 16);
-                    kp[p] = pack2(__uint_as_float(x0), __uint_as_float(x1));
-                }
+                    for (int p = 0; p < 7; ++p) {
+                        const uint32_t x0 = half ? bf16hi_f32(kv[2 * p]) : bf16lo_f32(kv[2 * p]);
+                        const uint32_t x1 = half ? bf16hi_f32(kv[2 * p + 1]) : bf16lo_f32(kv[2 * p + 1]);
+                        kp[p] = pack2u(x0, x1);
+                    }
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const uint32_t y = half ? (qv[a] & 0xFFFF0000u) : (qv[a] << 16);
-                    const unsigned long long qq = pack2(__uint_as_float(y), __uint_as_float(y));
+                    for (int a = 0; a < 4; ++a) {
+                        const uint32_t y = half ? bf16hi_f32(qv[a]) : bf16lo_f32(qv[a]);
+                        const unsigned long long qq2 = pack2u(y, y);
 #pragma unroll
-                    for (int p = 0; p < 7; ++p) ffma2(acc[a][p], qq, kp[p]);
+                        for (int p = 0; p < 7; ++p) ffma2(acc[a][p], qq2, kp[p]);
+                    }
                 }
             }
         }
@@ -187,11 +227,19 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     // ---- (row, block) tasks: block max
     for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
         const int r = task % kRows, s = task / kRows; // lanes = rows: conflict-free
-        double bm = -INFINITY;
-        if (s < nsl)
-            for (int t = 0; t < sm.blk_len[s]; ++t)
-                bm = fmax(bm, static_cast<double>(sm.u.logit[r][s * kBlockK + t]));
-        sm.bmax[r][s] = bm;
+        // max of fp32 logits in fp32 (exact; the double of the max float equals
+        // the reference's max over doubles), four chains, FP32 pipe not FP64
+        float bm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (s < nsl) {
+            const float *lg = &sm.u.logit[r][s * kBlockK];
+            if (sm.blk_len[s] == kBlockK) {
+#pragma unroll
+                for (int t = 0; t < kBlockK; ++t) bm4[t & 3] = fmaxf(bm4[t & 3], lg[t]);
+            } else {
+                for (int t = 0; t < sm.blk_len[s]; ++t) bm4[0] = fmaxf(bm4[0], lg[t]);
+            }
+        }
+        sm.bmax[r][s] = static_cast<double>(fmaxf(fmaxf(bm4[0], bm4[1]), fmaxf(bm4[2], bm4[3])));
     }
     __syncthreads();
     SALE_PHASE(4)
