@@ -31,7 +31,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "prefill attention ms & speedup vs dense at 64K/128K; estimation overhead % of dense"
-MODEL = dict(q_heads=32, kv_heads=8, head_dim=128)
+MODELS = {"llama": ("Llama-3.1-8B", dict(q_heads=32, kv_heads=8, head_dim=128)),
+          "qwen": ("Qwen2.5-7B", dict(q_heads=28, kv_heads=4, head_dim=128))}
+MODEL = dict(MODELS["llama"][1])  # the selected shape (parse() updates it)
 SAMPLE_TOKENS = 8192  # CPU sample: the first 8K tokens of the same workload
 
 
@@ -49,12 +51,32 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--seed", type=int, default=7)
-    return p.parse_args()
+    p.add_argument("--model", default="llama", choices=sorted(MODELS),
+                   help="attention shape: llama (32 Q / 8 KV heads) or qwen (28 / 4)")
+    p.add_argument("--second-tokens", type=int, default=65536,
+                   help="second sequence length reported beside the headline (0 = off)")
+    a = p.parse_args()
+    MODEL.clear()
+    MODEL.update(MODELS[a.model][1])
+    return a
 
 
-def workload_name(a):
-    return (f"Llama-3.1-8B attention layer (32 Q / 8 KV heads, d=128), B={a.batch}, "
-            f"seq {a.tokens}, causal, GQA sink_local synthetic (seed {a.seed}), tau={a.tau}")
+def workload_name(a, tokens=None):
+    name = MODELS[a.model][0]
+    return (f"{name} attention layer ({MODEL['q_heads']} Q / {MODEL['kv_heads']} KV heads, d=128), "
+            f"B={a.batch}, seq {tokens or a.tokens}, causal, GQA sink_local synthetic "
+            f"(seed {a.seed}), tau={a.tau}")
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t["kernels"][kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def dist_env():
@@ -179,7 +201,7 @@ def run_reference(a):
         walls.append(w)
     value = float(np.mean(vals))
     sample = (f"reference run_pipeline stages (quant+selection_pass+block_sparse_attention) on "
-              f"the first {ns} tokens of all 32 Q heads, {threads} threads, measured "
+              f"the first {ns} tokens of all {MODEL["q_heads"]} Q heads, {threads} threads, measured "
               f"{np.mean(walls):.0f} ms wall per sample; extrapolated to {a.tokens} tokens "
               f"(quant x N, selection/computation x N^2)")
     line = {"metric": METRIC, "value": value, "unit": "ms", "n_gpus": a.gpus, "steps": a.steps,
@@ -215,17 +237,11 @@ def run_b200(a):
         raise SystemExit(f"--gpus {world} must divide the {Hkv} KV heads")
     hkv = Hkv // world
     hq = hkv * (Hq // Hkv)
-    B, N = a.batch, a.tokens
+    B = a.batch
     threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE",
                                                                           world))))
-    q16, k16, v16 = sale.workload_gqa("sink_local", a.seed, B, N, hq, hkv, d, threads=threads,
-                                      kv_begin=rank * hkv)
-    dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
-    q, k, v = dev(q16), dev(k16), dev(v16)
-    taus = [a.tau] * hq
-    nq, nk, nw = sale.grid(N)
-    mask = torch.empty((B, hq, nq, nw), dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream()
+    dev = lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
 
     def barrier():
         torch.cuda.synchronize()
@@ -233,8 +249,8 @@ def run_b200(a):
             torch.distributed.barrier()
             torch.cuda.synchronize()
 
-    def timed(fn, steps):
-        for _ in range(a.warmup):
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
             fn()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -245,79 +261,110 @@ def run_b200(a):
         barrier()
         return e0.elapsed_time(e1) / steps
 
-    prefill = lambda: sale.prefill(q, k, v, taus, mask_out=mask)
-    dense = lambda: sale.block_sparse_attention(q, k, v, None)
+    def measure(N, steps, warmup, headline):
+        """One sequence length: prefill (headline: clocks, sweep, e2e), the
+        dense-mask run, per-stage times, density, algorithmic work. Per-rank
+        values; the caller reduces over ranks."""
+        q16, k16, v16 = sale.workload_gqa("sink_local", a.seed, B, N, hq, hkv, d, threads=threads,
+                                          kv_begin=rank * hkv)
+        q, k, v = dev(q16), dev(k16), dev(v16)
+        taus = [a.tau] * hq
+        nq, nk, nw = sale.grid(N)
+        mask = torch.empty((B, hq, nq, nw), dtype=torch.int32, device="cuda")
+        prefill = lambda: sale.prefill(q, k, v, taus, mask_out=mask)
+        dense = lambda: sale.block_sparse_attention(q, k, v, None)
+        r = {"N": N}
+        # ---- K full SALE prefills, device-timed (clocks sampled on the headline)
+        if headline:
+            with ClockSampler(local) as clocks:
+                r["ms"] = timed(prefill, steps, warmup)
+            r["clock"] = clocks.summary()
+        else:
+            r["ms"] = timed(prefill, steps, warmup)
+        # ---- dense-mask run of the same attention kernel
+        r["dense_ms"] = timed(dense, max(3, steps // 2), warmup)
+        # ---- per-stage times (events between the kernels inside the ABI)
+        sale.set_timing(True)
+        stages = []
+        for _ in range(max(3, steps // 2)):
+            prefill()
+            stages.append(sale.stage_times())
+        sale.set_timing(False)
+        r["stage_ms"] = {key: float(np.mean([st[key] for st in stages])) for key in stages[0]}
+        # ---- density and algorithmic work
+        counts = sale.flop_accounting(mask, N).cpu().numpy()
+        r["computed"], r["total"] = int(counts[..., 0].sum()), int(counts[..., 2].sum())
+        _, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True)
+        r["attended"] = int(cov.to(torch.int64).sum().item())
+        f_i = np.arange(nq)
+        r["est_blocks"] = B * hq * int(np.where(f_i >= 3, 4 * ((2 * f_i - 5) // 4), 0).sum())
+        if not headline:
+            return r
+        # ---- tau sweep (density vs latency)
+        r["sweep"] = []
+        taus_sweep = [float(x) for x in a.sweep.split(",") if x.strip()] if a.sweep else []
+        for t in taus_sweep:
+            tt = [t] * hq
+            ms_t = timed(lambda: sale.prefill(q, k, v, tt, mask_out=mask), 3, warmup)
+            c = sale.flop_accounting(mask, N).cpu().numpy()
+            r["sweep"].append({"tau": t, "density": float(c[..., 0].sum() / c[..., 2].sum()),
+                               "ms": ms_t})
+        # ---- e2e through the public host API (pinned buffers, copies timed)
+        r["e2e_ms"] = None
+        if not a.no_e2e:
+            del q, k, v
+            pin = lambda x: torch.from_numpy(x).pin_memory()
+            hq16, hk16, hv16 = pin(q16), pin(k16), pin(v16)
+            hout = torch.empty_like(hq16).pin_memory()
+            del q16, k16, v16
+            for _ in range(2):
+                sale.prefill_host(hq16, hk16, hv16, taus, hout)
+            barrier()
+            walls = []
+            for _ in range(max(3, steps // 2)):
+                t0 = time.perf_counter()
+                sale.prefill_host(hq16, hk16, hv16, taus, hout)
+                walls.append((time.perf_counter() - t0) * 1e3)
+            r["e2e_ms"] = float(np.mean(walls))
+            r["h2d"] = hq16.numel() * 2 + hk16.numel() * 2 + hv16.numel() * 2
+            r["d2h"] = hout.numel() * 2
+        return r
 
-    # ---- headline: K full SALE prefills, device-timed, clocks sampled
-    with ClockSampler(local) as clocks:
-        ms_step = timed(prefill, a.steps)
-    clock = clocks.summary()
-    # ---- dense-mask run of the same attention kernel
-    ms_dense = timed(dense, max(3, a.steps // 2))
-    # ---- per-stage times (events between the kernels inside the ABI)
-    sale.set_timing(True)
-    stages = []
-    for _ in range(max(3, a.steps // 2)):
-        prefill()
-        stages.append(sale.stage_times())
-    sale.set_timing(False)
-    stage_ms = {key: float(np.mean([s[key] for s in stages])) for key in stages[0]}
-    # ---- density and algorithmic work
-    counts = sale.flop_accounting(mask, N).cpu().numpy()
-    computed, total = int(counts[..., 0].sum()), int(counts[..., 2].sum())
-    _, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True)
-    attended = int(cov.to(torch.int64).sum().item())
-    attn_flops = 4.0 * d * attended                         # QK^T + PV, 2 flop per MAC
-    dense_flops = 4.0 * d * B * hq * N * (N + 1) / 2
-    f_i = np.arange(nq)
-    est_blocks = B * hq * int(np.where(f_i >= 3, 4 * ((2 * f_i - 5) // 4), 0).sum())
-    est_ops = 2.0 * 64 * 32 * 128 * est_blocks
+    def reduce_ranks(r):
+        """max over ranks for times, sum for counts (rank 0 gets the result)."""
+        keys = list(r["stage_ms"])
+        vec = torch.tensor([r["ms"], r["dense_ms"], r.get("e2e_ms") or 0.0] +
+                           [r["stage_ms"][k2] for k2 in keys], dtype=torch.float64, device="cuda")
+        tot = torch.tensor([r["computed"], r["total"], r["attended"], r["est_blocks"]],
+                           dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(vec, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
+        r["ms"], r["dense_ms"] = float(vec[0]), float(vec[1])
+        if r.get("e2e_ms") is not None:
+            r["e2e_ms"] = float(vec[2])
+        r["stage_ms"] = dict(zip(keys, [float(x) for x in vec[3:]]))
+        r["computed"], r["total"], r["attended"], r["est_blocks"] = (float(x) for x in tot)
+        r["density"] = r["computed"] / r["total"]
+        sel = r["stage_ms"]["base_mask"] + r["stage_ms"]["stats"] + r["stage_ms"]["estimate"]
+        r["overhead"] = (r["stage_ms"]["quantize"] + sel) / r["dense_ms"]
+        return r
 
-    # ---- tau sweep (density vs latency)
-    sweep = []
-    taus_sweep = [float(x) for x in a.sweep.split(",") if x.strip()] if a.sweep else []
-    for t in taus_sweep:
-        tt = [t] * hq
-        ms_t = timed(lambda: sale.prefill(q, k, v, tt, mask_out=mask), 3)
-        c = sale.flop_accounting(mask, N).cpu().numpy()
-        sweep.append({"tau": t, "density": float(c[..., 0].sum() / c[..., 2].sum()),
-                      "ms": ms_t})
-    # ---- e2e through the public host API (pinned buffers, copies timed)
-    e2e_ms = None
-    if not a.no_e2e:
-        pin = lambda x: torch.from_numpy(x).pin_memory()
-        hq16, hk16, hv16 = pin(q16), pin(k16), pin(v16)
-        hout = torch.empty_like(hq16).pin_memory()
-        del q16, k16, v16
-        for _ in range(2):
-            sale.prefill_host(hq16, hk16, hv16, taus, hout)
-        barrier()
-        walls = []
-        for _ in range(max(3, a.steps // 2)):
-            t0 = time.perf_counter()
-            sale.prefill_host(hq16, hk16, hv16, taus, hout)
-            walls.append((time.perf_counter() - t0) * 1e3)
-        e2e_ms = float(np.mean(walls))
-        h2d = hq16.numel() * 2 + hk16.numel() * 2 + hv16.numel() * 2
-        d2h = hout.numel() * 2
-    # ---- max over ranks
-    vec = torch.tensor([ms_step, ms_dense, e2e_ms or 0.0] + [stage_ms[k] for k in stage_ms],
-                       dtype=torch.float64, device="cuda")
-    tot = torch.tensor([computed, total, attended], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(vec, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
+    main_r = reduce_ranks(measure(a.tokens, a.steps, a.warmup, True))
+    second = None
+    if a.second_tokens and a.second_tokens != a.tokens:
+        second = reduce_ranks(measure(a.second_tokens, max(3, a.steps // 2), a.warmup, False))
     if rank != 0:
         torch.distributed.destroy_process_group()
         return
-    ms_step, ms_dense, e2e_ms = float(vec[0]), float(vec[1]), float(vec[2]) or None
-    stage_ms = dict(zip(stage_ms.keys(), [float(x) for x in vec[3:]]))
-    computed, total, attended = (float(x) for x in tot)
-    density = computed / total
-
+    N = a.tokens
+    ms_step, ms_dense, e2e_ms = main_r["ms"], main_r["dense_ms"], main_r.get("e2e_ms")
+    stage_ms, density, overhead = main_r["stage_ms"], main_r["density"], main_r["overhead"]
+    clock, sweep = main_r["clock"], main_r["sweep"]
+    attn_flops = 4.0 * d * main_r["attended"]                # QK^T + PV, 2 flop per MAC
+    dense_flops = 4.0 * d * B * Hq * N * (N + 1) / 2
+    est_ops = 2.0 * 64 * 32 * 128 * main_r["est_blocks"]
     peaks, peak_src = measured_peaks()
-    sel_ms = stage_ms["base_mask"] + stage_ms["stats"] + stage_ms["estimate"]
-    overhead = (stage_ms["quantize"] + sel_ms) / ms_dense
     dom = max(("attention", "estimate", "stats", "quantize"), key=lambda s: stage_ms[s])
     if dom == "attention":
         achieved = attn_flops / (stage_ms["attention"] * 1e-3) / 1e12
@@ -334,7 +381,11 @@ def run_b200(a):
         achieved, roof = 0.0, {"kernel": dom, "bound": "compute", "achieved": 0.0,
                                "peak": 1.0, "unit": "n/a"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    kname = roof["kernel"].split()[0]
+    tb = ncu_traffic(kname) if world == 1 and N == 131072 and B == 1 and a.model == "llama" else None
+    roof["traffic"] = tb / 1e9 if tb else None
+    if tb:
+        roof["traffic_unit"] = "GB per launch (dram read+write, ncu --set full, profiles/ncu_traffic.json)"
 
     line = {"metric": METRIC, "value": ms_step, "unit": "ms", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
@@ -343,15 +394,22 @@ def run_b200(a):
             "config": {"workload": workload_name(a), "tokens": N, "batch": B, "tau": a.tau,
                        "q_heads": Hq, "kv_heads": Hkv, "head_dim": d,
                        "parallelism": f"kv-group sharded x{world}, no collective",
-                       "l2": "inputs (1.5 GiB) larger than L2; no flush"},
+                       "l2": f"inputs ({B * N * (Hq + 2 * Hkv) * d * 2 / 2**30:.2f} GiB) larger "
+                             "than L2; no flush"},
             "speedup_vs_dense": ms_dense / ms_step, "dense_ms": ms_dense,
             "estimation_overhead_pct": 100.0 * overhead, "density": density,
             "stage_ms": stage_ms, "effective_tflops": dense_flops * world / (ms_step * 1e-3) / 1e12,
             "tau_sweep": sweep, "roofline": roof, "clocks": clock,
             "gpu_launches": 5 * a.steps}
+    if second is not None:
+        line["at_%dk" % (second["N"] // 1024)] = {
+            "tokens": second["N"], "ms": second["ms"], "dense_ms": second["dense_ms"],
+            "speedup_vs_dense": second["dense_ms"] / second["ms"],
+            "estimation_overhead_pct": 100.0 * second["overhead"], "density": second["density"],
+            "stage_ms": second["stage_ms"]}
     if e2e_ms is not None:
-        line["e2e"] = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(h2d) * world,
-                       "d2h_bytes_per_step": int(d2h) * world,
+        line["e2e"] = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(main_r["h2d"]) * world,
+                       "d2h_bytes_per_step": int(main_r["d2h"]) * world,
                        "api": "sale_b200_prefill_host (pinned host buffers)"}
     if world == 1 and not a.no_cpu_baseline:
         try:
@@ -361,7 +419,7 @@ def run_b200(a):
             line["cpu_baseline"] = {
                 "value": v, "unit": "ms", "cores": threads, "kind": "reference",
                 "sample": f"reference quant+selection_pass+block_sparse_attention on the first "
-                          f"{ns} tokens of all 32 Q heads ({w:.0f} ms wall, {threads} threads), "
+                          f"{ns} tokens of all {MODEL["q_heads"]} Q heads ({w:.0f} ms wall, {threads} threads), "
                           f"extrapolated to {N} tokens (quant x N, rest x N^2)"}
         except Exception as e:  # the oracle is a reported baseline, never the product
             line["cpu_baseline"] = {"value": None, "unavailable": str(e)}

@@ -18,16 +18,20 @@ namespace sale_b200 {
 
 namespace {
 
-__device__ __forceinline__ int8_t quantize_one(float x, float scale, float inv_scale) {
+// Code of one element, returned as its int8 bit pattern in the low byte. All
+// float arithmetic (FMA / ALU pipes): no float<->int conversions, which run on
+// the quarter-rate XU pipe.
+__device__ __forceinline__ uint32_t quantize_one(float x, float scale, float inv_scale) {
+    constexpr float kMagic = 12582912.0f; // 1.5 * 2^23: x + kMagic rounds x to an integer
     const float a = fabsf(x);
-    int k = static_cast<int>(a * inv_scale + 0.5f);
-    k = k > 7 ? 7 : k;
-    if (k > 0 && fmaf(static_cast<float>(2 * k - 1), scale, -2.0f * a) > 0.0f) {
-        --k; // a < (k - 1/2) * scale
-    } else if (k < 7 && fmaf(static_cast<float>(2 * k + 1), scale, -2.0f * a) <= 0.0f) {
-        ++k; // a >= (k + 1/2) * scale: ties go away from zero
-    }
-    return static_cast<int8_t>(x < 0.0f ? -k : k);
+    float k = fminf((a * inv_scale + kMagic) - kMagic, 7.0f); // within one of the exact code
+    // exact corrections: a < (k - 1/2) * scale -> k - 1; a >= (k + 1/2) * scale
+    // -> k + 1 (ties go away from zero); the fmaf sign is exact
+    const bool down = k > 0.0f && fmaf(2.0f * k - 1.0f, scale, -2.0f * a) > 0.0f;
+    const bool up = k < 7.0f && fmaf(2.0f * k + 1.0f, scale, -2.0f * a) <= 0.0f;
+    k += up ? 1.0f : (down ? -1.0f : 0.0f);
+    // integer -7..7 -> two's complement byte in the low mantissa bits
+    return static_cast<uint32_t>(__float_as_int((x < 0.0f ? -k : k) + kMagic)) & 0xFFu;
 }
 
 __device__ __forceinline__ void unpack8(const uint4 &u, float (&f)[8]) {
@@ -39,12 +43,10 @@ __device__ __forceinline__ void unpack8(const uint4 &u, float (&f)[8]) {
     }
 }
 
-__device__ __forceinline__ uint2 pack8(const int8_t (&c)[8]) {
+__device__ __forceinline__ uint2 pack8(const uint32_t (&c)[8]) {
     uint2 r;
-    r.x = (uint32_t)(uint8_t)c[0] | ((uint32_t)(uint8_t)c[1] << 8) |
-          ((uint32_t)(uint8_t)c[2] << 16) | ((uint32_t)(uint8_t)c[3] << 24);
-    r.y = (uint32_t)(uint8_t)c[4] | ((uint32_t)(uint8_t)c[5] << 8) |
-          ((uint32_t)(uint8_t)c[6] << 16) | ((uint32_t)(uint8_t)c[7] << 24);
+    r.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
+    r.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
     return r;
 }
 
@@ -53,11 +55,14 @@ __device__ __forceinline__ float scale_of(float peak) {
 }
 
 constexpr int kThreads = 256;
-constexpr int kRowsPerCta = 16;   // Q: 16 lanes x 8 elements per 128-wide row
-constexpr int kLanesPerRow = 16;
+constexpr int kLanesPerRow = 16;  // Q: 16 lanes x 8 elements per 128-wide row
+constexpr int kQSlots = 4;        // Q rows per 16-lane group in flight (4 x 16 B loads per thread)
+constexpr int kQRowsPerCta = kThreads / kLanesPerRow * kQSlots; // 64
 
-// One CTA = 16 Q rows (consecutive (b, n, h) rows) or one K group
-// (b, key block j, kv head h): 32 rows x 128, 16 elements per thread.
+// CTAs [0, q_ctas): 64 consecutive Q rows ((b, n, h) order), every thread
+// loading its four 16-byte chunks before any math (memory-level parallelism);
+// CTAs [q_ctas, ...): one K group (b, key block j, kv head h) = 32 rows x 128,
+// 16 elements per thread. Scales need only 32-bit index math (rows < 2^31).
 __global__ void __launch_bounds__(kThreads)
 quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__restrict__ k,
                    int8_t *__restrict__ q_codes, float *__restrict__ q_scales,
@@ -66,40 +71,50 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
     const int tid = threadIdx.x;
     if (blockIdx.x < q_ctas) {
         const int64_t q_rows = batch * tokens * hq;
-        const int64_t row = static_cast<int64_t>(blockIdx.x) * kRowsPerCta + tid / kLanesPerRow;
         const int sub = tid % kLanesPerRow;
-        float f[8];
-        float peak = 0.0f;
-        if (row < q_rows) {
-            const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(q + row * kHeadDim) + sub);
-            unpack8(u, f);
+        const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kQRowsPerCta + tid / kLanesPerRow;
+        uint4 u[kQSlots];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) peak = fmaxf(peak, fabsf(f[i]));
+        for (int sl = 0; sl < kQSlots; ++sl) {
+            const int64_t row = row0 + sl * (kThreads / kLanesPerRow);
+            u[sl] = row < q_rows ? __ldcs(reinterpret_cast<const uint4 *>(q + row * kHeadDim) + sub)
+                                 : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
-        if (row >= q_rows) return;
-        const float scale = scale_of(peak);
-        const float inv = 1.0f / scale;
-        int8_t c[8];
+        for (int sl = 0; sl < kQSlots; ++sl) {
+            const int64_t row = row0 + sl * (kThreads / kLanesPerRow);
+            float f[8];
+            unpack8(u[sl], f);
+            float peak = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] = quantize_one(f[i], scale, inv);
-        __stcs(reinterpret_cast<uint2 *>(q_codes + row * kHeadDim) + sub, pack8(c));
-        if (sub == 0) {
-            // row = (b*N + n)*Hq + h  ->  scales[b][h][n]
-            const int64_t h = row % hq;
-            const int64_t bn = row / hq;
-            const int64_t b = bn / tokens, n = bn % tokens;
-            q_scales[(b * hq + h) * tokens + n] = scale;
+            for (int i = 0; i < 8; ++i) peak = fmaxf(peak, fabsf(f[i]));
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+            if (row >= q_rows) continue;
+            const float scale = scale_of(peak);
+            const float inv = 1.0f / scale;
+            uint32_t c[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) c[i] = quantize_one(f[i], scale, inv);
+            __stcs(reinterpret_cast<uint2 *>(q_codes + row * kHeadDim) + sub, pack8(c));
+            if (sub == 0) {
+                // row = (b*N + n)*Hq + h  ->  scales[b][h][n]
+                const uint32_t r32 = static_cast<uint32_t>(row), hq32 = static_cast<uint32_t>(hq);
+                const uint32_t h = r32 % hq32, bn = r32 / hq32;
+                const uint32_t n32 = static_cast<uint32_t>(tokens);
+                const uint32_t b = bn / n32, n = bn % n32;
+                q_scales[(static_cast<int64_t>(b) * hq + h) * tokens + n] = scale;
+            }
         }
         return;
     }
     // ---- K group
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
-    const int64_t grp = static_cast<int64_t>(blockIdx.x) - q_ctas;
-    const int64_t h = grp % hkv;
-    const int64_t j = (grp / hkv) % nk;
-    const int64_t b = grp / (hkv * nk);
+    const uint32_t grp = static_cast<uint32_t>(static_cast<int64_t>(blockIdx.x) - q_ctas);
+    const uint32_t hkv32 = static_cast<uint32_t>(hkv), nk32 = static_cast<uint32_t>(nk);
+    const int64_t h = grp % hkv32;
+    const int64_t j = (grp / hkv32) % nk32;
+    const int64_t b = grp / (hkv32 * nk32);
     const int r = tid >> 3;         // token within the block (0..31)
     const int sub = (tid & 7) * 2;  // two 8-element chunks: 16 elements
     const int64_t tok = j * kBlockK + r;
@@ -109,8 +124,9 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
     float peak = 0.0f;
     if (valid) {
         const uint4 *src = reinterpret_cast<const uint4 *>(k + row * kHeadDim) + sub;
-        unpack8(__ldcs(src), f0);
-        unpack8(__ldcs(src + 1), f1);
+        const uint4 u0 = __ldcs(src), u1 = __ldcs(src + 1);
+        unpack8(u0, f0);
+        unpack8(u1, f1);
 #pragma unroll
         for (int i = 0; i < 8; ++i) peak = fmaxf(peak, fmaxf(fabsf(f0[i]), fabsf(f1[i])));
     }
@@ -125,7 +141,7 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
     const float scale = scale_of(peak);
     const float inv = 1.0f / scale;
     if (valid) {
-        int8_t c0[8], c1[8];
+        uint32_t c0[8], c1[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             c0[i] = quantize_one(f0[i], scale, inv);
@@ -144,7 +160,8 @@ cudaError_t launch_quantize_qk(const void *q, const void *k, int8_t *q_codes, fl
                                int8_t *k_codes, float *k_scales, int64_t batch, int64_t tokens,
                                int64_t hq, int64_t hkv, cudaStream_t stream) {
     const int64_t q_rows = q ? batch * tokens * hq : 0;
-    const int64_t q_ctas = (q_rows + kRowsPerCta - 1) / kRowsPerCta;
+    const int64_t q_ctas = (q_rows + kQRowsPerCta - 1) / kQRowsPerCta;
+    if (q_rows > 0x7FFFFFFF) return cudaErrorInvalidValue; // 32-bit scale index math
     const int64_t k_ctas = k ? batch * ((tokens + kBlockK - 1) / kBlockK) * hkv : 0;
     const int64_t grid = q_ctas + k_ctas;
     if (grid == 0) return cudaSuccess;

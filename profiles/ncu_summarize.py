@@ -1,0 +1,45 @@
+"""Per-kernel summary table (markdown) + DRAM traffic json from an
+`ncu --set full` report: python profiles/ncu_summarize.py rep.ncu-rep out.md out.json"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
+           "launch__grid_size", "launch__block_size"]
+rep, out_md, out_json = sys.argv[1:4]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units, data = rows[0], rows[1], rows[2:]
+ix = {h: i for i, h in enumerate(hdr)}
+name = lambda r: r[ix["Kernel Name"]].split("(")[0].split("::")[-1]
+lines = ["| kernel | " + " | ".join(f"{m} ({units[ix[m]]})" for m in METRICS) + " |",
+         "|---|" + "---|" * len(METRICS)]
+traffic = {}
+seen = {}
+for r in data:
+    n = name(r)
+    seen[n] = seen.get(n, 0) + 1
+    label = n if seen[n] == 1 else f"{n} #{seen[n]}"
+    lines.append(f"| {label} | " + " | ".join(r[ix[m]] for m in METRICS) + " |")
+    if seen[n] == 1:  # first launch of each kernel: the sparse (bench) launch
+        def val(m):
+            v, u = float(r[ix[m]].replace(",", "")), units[ix[m]]
+            return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        traffic[n] = {"dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+                      "duration_ms_under_ncu": float(r[ix["gpu__time_duration.sum"]]) *
+                      {"ms": 1, "us": 1e-3, "ns": 1e-6}.get(units[ix["gpu__time_duration.sum"]], 1)}
+open(out_md, "w").write("\n".join(lines) + "\n")
+json.dump({"source": rep.split("/")[-1], "kernels": traffic}, open(out_json, "w"), indent=1)
+print("\n".join(lines))
