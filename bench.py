@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--seed", type=int, default=7)
     p.add_argument("--model", default="llama", choices=sorted(MODELS),
                    help="attention shape: llama (32 Q / 8 KV heads) or qwen (28 / 4)")
+    p.add_argument("--gather", action="store_true",
+                   help="N>1: also time the optional NCCL all_gather of O (not on the critical path)")
     p.add_argument("--second-tokens", type=int, default=65536,
                    help="second sequence length reported beside the headline (0 = off)")
     a = p.parse_args()
@@ -300,6 +302,10 @@ def run_b200(a):
         r["est_blocks"] = B * hq * int(np.where(f_i >= 3, 4 * ((2 * f_i - 5) // 4), 0).sum())
         if not headline:
             return r
+        # ---- optional output gather over NCCL (timed separately, max over ranks)
+        if a.gather and world > 1:
+            out = prefill()
+            r["gather_ms"] = timed(lambda: sale.gather_heads(out), 3, 1)
         # ---- tau sweep (density vs latency)
         r["sweep"] = []
         taus_sweep = [float(x) for x in a.sweep.split(",") if x.strip()] if a.sweep else []
@@ -333,7 +339,7 @@ def run_b200(a):
     def reduce_ranks(r):
         """max over ranks for times, sum for counts (rank 0 gets the result)."""
         keys = list(r["stage_ms"])
-        vec = torch.tensor([r["ms"], r["dense_ms"], r.get("e2e_ms") or 0.0] +
+        vec = torch.tensor([r["ms"], r["dense_ms"], r.get("e2e_ms") or 0.0, r.get("gather_ms", 0.0)] +
                            [r["stage_ms"][k2] for k2 in keys], dtype=torch.float64, device="cuda")
         tot = torch.tensor([r["computed"], r["total"], r["attended"], r["est_blocks"]],
                            dtype=torch.float64, device="cuda")
@@ -343,7 +349,9 @@ def run_b200(a):
         r["ms"], r["dense_ms"] = float(vec[0]), float(vec[1])
         if r.get("e2e_ms") is not None:
             r["e2e_ms"] = float(vec[2])
-        r["stage_ms"] = dict(zip(keys, [float(x) for x in vec[3:]]))
+        if "gather_ms" in r:
+            r["gather_ms"] = float(vec[3])
+        r["stage_ms"] = dict(zip(keys, [float(x) for x in vec[4:]]))
         r["computed"], r["total"], r["attended"], r["est_blocks"] = (float(x) for x in tot)
         r["density"] = r["computed"] / r["total"]
         sel = r["stage_ms"]["base_mask"] + r["stage_ms"]["stats"] + r["stage_ms"]["estimate"]
@@ -401,6 +409,8 @@ def run_b200(a):
             "stage_ms": stage_ms, "effective_tflops": dense_flops * world / (ms_step * 1e-3) / 1e12,
             "tau_sweep": sweep, "roofline": roof, "clocks": clock,
             "gpu_launches": 5 * a.steps}
+    if "gather_ms" in main_r:
+        line["output_gather_ms"] = main_r["gather_ms"]
     if second is not None:
         line["at_%dk" % (second["N"] // 1024)] = {
             "tokens": second["N"], "ms": second["ms"], "dense_ms": second["dense_ms"],

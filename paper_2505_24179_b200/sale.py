@@ -318,6 +318,22 @@ def prefill_host(q, k, v, taus, out, head_dim=128, config=None):
     return out
 
 
+# ------------------------------------------------------------- multi-GPU
+
+def gather_heads(out_shard, group=None):
+    """The optional output gather of a KV-group-sharded prefill (SURVEY.md
+    §8(e)): every rank holds O for its contiguous slice of query heads,
+    [B, N, Hq/world, d]; all_gather (NCCL over NVLink on GPUs, gloo on CPU)
+    and concatenate along the head axis -> [B, N, Hq, d] on every rank. Not on
+    the critical path: the three SALE stages never exchange data."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(out_shard) for _ in range(world)]
+    dist.all_gather(parts, out_shard.contiguous(), group=group)
+    return torch.cat(parts, dim=2)
+
+
 # ------------------------------------------------------------- workloads
 
 def workload_head_f32(kind: str, seed: int, tokens: int, dim: int, head: int = 0):

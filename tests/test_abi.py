@@ -148,6 +148,36 @@ def _gloo_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def _gather_worker(rank, world, port, q):
+    import torch.distributed as dist
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(3)
+    full = torch.randn(2, 64, 8, 16, generator=g)       # [B, N, Hq, d]
+    shard = full[:, :, 4 * rank:4 * rank + 4].clone()   # this rank's query heads
+    got = sale.gather_heads(shard)
+    q.put((rank, bool(torch.equal(got, full))))
+    dist.destroy_process_group()
+
+
+def test_output_gather_two_ranks_gloo():
+    """The optional output gather (sale.gather_heads): head-sliced shards of O
+    concatenate back to the full [B, N, Hq, d] on every rank."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    assert res == [(0, True), (1, True)]
+
+
 def test_kv_group_sharding_two_ranks_gloo():
     """bench.py's N>1 host path: each rank generates and owns a disjoint KV-group
     shard (no data-path collective); only timings are reduced (max)."""
