@@ -13,6 +13,10 @@
  *   4  SALE_B200_CUDA_ERROR
  *   5  SALE_B200_UNSUPPORTED        (valid for the reference, not on this path:
  *                                    see DESIGN.md "Scope")
+ *   6  SALE_B200_FORMAT_ERROR       (reference throws sale::TensorFileError; the
+ *                                    message carries "(offset N)" like its what())
+ *   7  SALE_B200_IO_ERROR           (reference throws std::runtime_error: cannot
+ *                                    open / write failed)
  *
  * Device data layout (all device pointers, caller-allocated):
  *   q            bf16 [B][N][Hq][128]      rows padded with zeros past head_dim
@@ -46,6 +50,8 @@ extern "C" {
 #define SALE_B200_OUT_OF_RANGE 3
 #define SALE_B200_CUDA_ERROR 4
 #define SALE_B200_UNSUPPORTED 5
+#define SALE_B200_FORMAT_ERROR 6
+#define SALE_B200_IO_ERROR 7
 
 typedef struct sale_b200_ctx sale_b200_ctx;
 
@@ -140,6 +146,108 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
 int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t *k,
                            const uint16_t *v, const sale_b200_shape *shape, const double *taus,
                            const sale_b200_selection_config *cfg, uint16_t *out);
+
+/* ---- orchestration above the stages (runner.hpp, calibrate.hpp) ---------- */
+
+/* l1_error (calibrate.hpp:20-29) for every (batch, q head): sum over tokens and
+ * the first head_dim channels of |ref - approx| in double, divided by the
+ * token count. ref / approx: device bf16 [B][N][Hq][128] (e.g. the dense and the
+ * sparse output). out: HOST double [B*Hq]. Synchronous. */
+int sale_b200_l1_error(sale_b200_ctx *ctx, const void *ref, const void *approx,
+                       const sale_b200_shape *shape, double *out);
+
+/* One head of a RunReport (report.hpp:12-23). */
+typedef struct {
+    int64_t head;             /* b * Hq + h */
+    double tau;
+    double sparsity;          /* skipped / total causal blocks */
+    double err;               /* l1_error(dense, sparse) */
+    int64_t computed_blocks, skipped_blocks, total_blocks;
+    int64_t coverage_min, coverage_max;
+    double coverage_mean;
+} sale_b200_head_report;
+/* StageTiming (report.hpp:26-38), device-event times of the whole batch. */
+typedef struct {
+    double quantization_ms, selection_ms, computation_ms, dense_ms;
+} sale_b200_stage_timing;
+
+/* run_pipeline (runner.hpp:37-108) for every (batch, q head) at once:
+ * quantization, selection (or the all-true mask when dense_mask != 0, i.e.
+ * RunOptions::dense_mask), block-sparse computation with coverage, the dense
+ * baseline, flop accounting, l1 error and coverage statistics. q/k/v device;
+ * taus HOST [Hq]; reports HOST [B*Hq]; timing HOST (may be NULL). Synchronous. */
+int sale_b200_run_pipeline(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                           const sale_b200_shape *shape, const double *taus,
+                           const sale_b200_selection_config *cfg, int dense_mask,
+                           sale_b200_head_report *reports, sale_b200_stage_timing *timing);
+
+/* SweepRow (runner.hpp:110-114). */
+typedef struct {
+    double tau;
+    double sparsity; /* mean over all (batch, q head) */
+    double err;      /* max over all (batch, q head) */
+} sale_b200_sweep_row;
+/* sweep_thresholds (runner.hpp:119-165): quantization and the dense baseline
+ * once, then per tau (applied to every head) selection + sparse computation +
+ * accounting + l1. taus HOST [n_taus] in (0,1); rows HOST [n_taus]. */
+int sale_b200_sweep_thresholds(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                               const sale_b200_shape *shape, const double *taus, int64_t n_taus,
+                               const sale_b200_selection_config *cfg, sale_b200_sweep_row *rows);
+
+/* CalibrationSettings (calibrate.hpp:56-68) minus the selection geometry. */
+typedef struct {
+    double theta;         /* 0.4   */
+    double tau0;          /* 0.008 */
+    int64_t max_halvings; /* 30    */
+} sale_b200_calibration_settings;
+/* HeadCalibration (calibrate.hpp:38-44); flag 0 converged, 1 floor-reached. */
+typedef struct {
+    int64_t layer, head;
+    double tau;
+    int32_t flag;
+    int64_t halvings;
+} sale_b200_head_calibration;
+/* calibrate_model (calibrate.hpp:149-175) with calibrate_head's greedy halving
+ * ladder (:121-145) for every q head at once: sample s is the device q/k/v
+ * triple q_samples[s], k_samples[s], v_samples[s] (batch must be 1; all samples
+ * share the shape). Quantization and the dense baseline are computed once per
+ * sample; every rung runs selection + sparse computation + l1 for all heads
+ * with per-head taus; a head stops at its first tau whose worst-sample error
+ * is <= theta. out HOST [Hq] (head = q head index, layer = 0). Synchronous. */
+int sale_b200_calibrate(sale_b200_ctx *ctx, const void *const *q_samples,
+                        const void *const *k_samples, const void *const *v_samples,
+                        int64_t n_samples, const sale_b200_shape *shape,
+                        const sale_b200_calibration_settings *settings,
+                        const sale_b200_selection_config *cfg, sale_b200_head_calibration *out);
+
+/* ---- file formats (host; docs/formats.md; errors: sale_b200_last_error(NULL)) */
+
+/* .tns header (tensor_file.hpp:98-125): heads, tokens, dim and dtype tag (1 =
+ * float32 as in the reference; 2 = bf16, this path's extension). */
+int sale_b200_tensor_file_info(const char *path, uint32_t *heads, uint32_t *tokens,
+                               uint32_t *dim, uint32_t *dtype);
+/* read_tensor_file (tensor_file.hpp:98-158) into this path's layout: HOST bf16
+ * [1][N][heads][128] q, k, v (RNE from float32, rows zero-padded past dim),
+ * i.e. an MHA shape (kv_heads = q_heads). Same validation and error offsets as
+ * the reference (magic, version, dtype, zero counts, truncation, non-finite
+ * values, trailing bytes). */
+int sale_b200_tensor_file_read_bf16(const char *path, uint16_t *q, uint16_t *k, uint16_t *v);
+/* write_tensor_file (tensor_file.hpp:69-96) from HOST bf16 [1][N][heads][128]:
+ * dtype 1 writes the bf16 values as float32 (byte-identical to the reference
+ * writer for bf16-valued inputs), dtype 2 writes bf16 payloads. */
+int sale_b200_tensor_file_write(const char *path, const uint16_t *q, const uint16_t *k,
+                                const uint16_t *v, uint32_t heads, uint32_t tokens, uint32_t dim,
+                                uint32_t dtype);
+/* write_mask_dump (mask_io.hpp:28-69) from packed HOST mask words
+ * [B][Hq][ceil(N/64)][W]: one RLE record per (batch, head), head index
+ * b * Hq + h, tau taus[b * Hq + h] (float32). Byte-identical to the reference. */
+int sale_b200_mask_dump_write(const char *path, const uint32_t *mask_words, int64_t batch,
+                              int64_t heads, int64_t tokens, const float *taus);
+/* read_mask_dump (mask_io.hpp:71-125) back into packed HOST words: first call
+ * with mask_words == NULL to get the record count and the grid (all records
+ * must share nq / nk); heads / taus receive each record's head index and tau. */
+int sale_b200_mask_dump_read(const char *path, int64_t *records, int64_t *nq, int64_t *nk,
+                             uint32_t *mask_words, uint32_t *heads, float *taus);
 
 /* ---- device memory helpers (so host code needs no CUDA headers) -----------
  * Synchronous allocation / copies on ctx's device. */

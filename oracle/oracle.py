@@ -97,6 +97,13 @@ def _load_ref():
     lib.ref_run_pipeline.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, i64, f64p,
                                      f64p, f64p]
     lib.ref_sale_heads.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, i64, f64p, f64p]
+    lib.ref_run_report.argtypes = [f32p, f32p, f32p, i64, i64, i64, f64p, C.c_int, i64, f64p]
+    lib.ref_sweep.argtypes = [f32p, f32p, f32p, i64, i64, i64, f64p, i64, i64, f64p]
+    lib.ref_calibrate_head.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, C.c_double, i64,
+                                       f64p, C.POINTER(C.c_int32), i64p]
+    lib.ref_write_tensor_file.argtypes = [C.c_char_p, f32p, f32p, f32p, i64, i64, i64]
+    lib.ref_read_tensor_file.argtypes = [C.c_char_p, f32p, f32p, f32p, C.c_char_p, i64]
+    lib.ref_write_mask_dump.argtypes = [C.c_char_p, u8p, C.POINTER(C.c_uint32), f32p, i64, i64, i64]
     return lib
 
 

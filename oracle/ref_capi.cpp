@@ -8,6 +8,9 @@
 // and as the reference CPU arm of bench.py (--impl reference / cpu_baseline).
 #include <sale/attention.hpp>
 #include <sale/block_grid.hpp>
+#include <sale/calibrate.hpp>
+#include <sale/mask_io.hpp>
+#include <sale/tensor_file.hpp>
 #include <sale/quant.hpp>
 #include <sale/runner.hpp>
 #include <sale/selection.hpp>
@@ -16,6 +19,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 #include <vector>
@@ -282,6 +286,113 @@ int ref_sale_heads(const float *q, const float *k, const float *v, int64_t heads
             stage_ms[i] = 0.0;
             for (int64_t h = 0; h < heads; ++h) stage_ms[i] += st[3 * h + i];
         }
+    });
+}
+
+// run_pipeline (runner.hpp:37) with per-head taus; every HeadReport field
+// (report.hpp:12-23) as doubles: out[h*10 + {0 sparsity, 1 err, 2 computed,
+// 3 skipped, 4 total, 5 cov_min, 6 cov_max, 7 cov_mean}].
+int ref_run_report(const float *q, const float *k, const float *v, int64_t heads, int64_t n,
+                   int64_t d, const double *taus, int dense_mask, int64_t threads, double *out) {
+    return guarded([&] {
+        std::vector<HeadInput> hs;
+        for (int64_t h = 0; h < heads; ++h)
+            hs.push_back(to_head(q + h * n * d, k + h * n * d, v + h * n * d, n, d));
+        const std::vector<double> tv(taus, taus + heads);
+        RunOptions opt;
+        opt.threads = static_cast<std::size_t>(threads);
+        opt.dense_mask = dense_mask != 0;
+        const RunReport r = run_pipeline(hs, tv, SelectionConfig{}, opt);
+        for (int64_t h = 0; h < heads; ++h) {
+            const HeadReport &x = r.head_reports[h];
+            double *o = out + 10 * h;
+            o[0] = x.sparsity, o[1] = x.err, o[2] = double(x.computed_blocks),
+            o[3] = double(x.skipped_blocks), o[4] = double(x.total_blocks);
+            o[5] = double(x.coverage_min), o[6] = double(x.coverage_max), o[7] = x.coverage_mean;
+        }
+    });
+}
+
+// sweep_thresholds (runner.hpp:119): rows[t*3 + {tau, sparsity, err}].
+int ref_sweep(const float *q, const float *k, const float *v, int64_t heads, int64_t n, int64_t d,
+              const double *taus, int64_t n_taus, int64_t threads, double *rows) {
+    return guarded([&] {
+        std::vector<HeadInput> hs;
+        for (int64_t h = 0; h < heads; ++h)
+            hs.push_back(to_head(q + h * n * d, k + h * n * d, v + h * n * d, n, d));
+        const std::vector<double> tv(taus, taus + n_taus);
+        const auto r = sweep_thresholds(hs, tv, SelectionConfig{}, static_cast<std::size_t>(threads));
+        for (int64_t t = 0; t < n_taus; ++t) {
+            rows[3 * t] = r[t].tau, rows[3 * t + 1] = r[t].sparsity, rows[3 * t + 2] = r[t].err;
+        }
+    });
+}
+
+// calibrate_head (calibrate.hpp:121) over samples laid out [s][n][d].
+int ref_calibrate_head(const float *q, const float *k, const float *v, int64_t samples, int64_t n,
+                       int64_t d, double theta, double tau0, int64_t max_halvings, double *tau,
+                       int32_t *flag, int64_t *halvings) {
+    return guarded([&] {
+        std::vector<HeadInput> hs;
+        for (int64_t s = 0; s < samples; ++s)
+            hs.push_back(to_head(q + s * n * d, k + s * n * d, v + s * n * d, n, d));
+        CalibrationSettings st;
+        st.theta = theta;
+        st.tau0 = tau0;
+        st.max_halvings = static_cast<std::size_t>(max_halvings);
+        const HeadCalibration c = calibrate_head(hs, st);
+        *tau = c.tau;
+        *flag = c.flag == CalibrationFlag::Converged ? 0 : 1;
+        *halvings = static_cast<int64_t>(c.halvings);
+    });
+}
+
+// write_tensor_file (tensor_file.hpp:69), heads laid out [h][n][d].
+int ref_write_tensor_file(const char *path, const float *q, const float *k, const float *v,
+                          int64_t heads, int64_t n, int64_t d) {
+    return guarded([&] {
+        std::vector<HeadInput> hs;
+        for (int64_t h = 0; h < heads; ++h)
+            hs.push_back(to_head(q + h * n * d, k + h * n * d, v + h * n * d, n, d));
+        write_tensor_file(path, hs);
+    });
+}
+
+// read_tensor_file (tensor_file.hpp:98): 0 and the values ([h][n][d] q, k, v)
+// or 6 with the TensorFileError what() in msg.
+int ref_read_tensor_file(const char *path, float *q, float *k, float *v, char *msg, int64_t cap) {
+    try {
+        const auto hs = read_tensor_file(path);
+        const std::size_t nd = hs.front().query.data().size();
+        for (std::size_t h = 0; h < hs.size(); ++h) {
+            std::memcpy(q + h * nd, hs[h].query.data().data(), 4 * nd);
+            std::memcpy(k + h * nd, hs[h].key.data().data(), 4 * nd);
+            std::memcpy(v + h * nd, hs[h].value.data().data(), 4 * nd);
+        }
+        return 0;
+    } catch (const TensorFileError &e) {
+        std::snprintf(msg, static_cast<std::size_t>(cap), "%s", e.what());
+        return 6;
+    } catch (const std::exception &e) {
+        std::snprintf(msg, static_cast<std::size_t>(cap), "%s", e.what());
+        return 7;
+    }
+}
+
+// write_mask_dump (mask_io.hpp:28) from uint8 cells [r][nq][nk].
+int ref_write_mask_dump(const char *path, const uint8_t *cells, const uint32_t *heads,
+                        const float *taus, int64_t records, int64_t nq, int64_t nk) {
+    return guarded([&] {
+        std::vector<MaskRecord> recs(static_cast<std::size_t>(records));
+        for (int64_t r = 0; r < records; ++r) {
+            recs[r].head = heads[r];
+            recs[r].tau = taus[r];
+            recs[r].mask = BlockMask(static_cast<std::size_t>(nq), static_cast<std::size_t>(nk));
+            for (int64_t i = 0; i < nq; ++i)
+                for (int64_t j = 0; j < nk; ++j)
+                    if (cells[(r * nq + i) * nk + j]) recs[r].mask.set(i, j, true);
+        }
+        write_mask_dump(path, recs);
     });
 }
 

@@ -44,7 +44,7 @@ struct sale_b200_ctx {
 
 namespace {
 
-std::string g_create_error;
+thread_local std::string g_create_error; // ctx-less calls (create, file formats)
 
 int fail(sale_b200_ctx *ctx, int code, const std::string &msg) {
     if (ctx) ctx->err = msg;
@@ -291,6 +291,11 @@ int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 } // namespace
+
+namespace sale_b200 {
+int set_error(sale_b200_ctx *ctx, int code, const std::string &msg) { return fail(ctx, code, msg); }
+int ctx_device_of(const sale_b200_ctx *ctx) { return ctx->device; }
+} // namespace sale_b200
 
 extern "C" {
 

@@ -5,7 +5,16 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <string>
+
+struct sale_b200_ctx;
+
 namespace sale_b200 {
+
+// capi.cu: record an error on ctx (or the calling thread's ctx-less slot when
+// ctx is NULL) and return code; ctx's device.
+int set_error(sale_b200_ctx *ctx, int code, const std::string &msg);
+int ctx_device_of(const sale_b200_ctx *ctx);
 
 struct EstUnit {
     int m;    // 128-row query tile: rows [128m+64, 128m+192) = query blocks 2m+1, 2m+2

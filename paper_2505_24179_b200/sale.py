@@ -48,8 +48,47 @@ class SelectDebug(C.Structure):
     _fields_ = [("running_max", vp), ("exp_sum", vp), ("bound", vp), ("block_max", vp)]
 
 
+class TensorFileError(RuntimeError):
+    """sale::TensorFileError (tensor_file.hpp:22-33): format error; `offset` is
+    the byte offset the message names."""
+
+    def __init__(self, message: str):
+        super().__init__(message)
+        import re
+        m = re.search(r"\(offset (\d+)\)$", message)
+        self.offset = int(m.group(1)) if m else None
+
+
+class HeadReport(C.Structure):
+    """sale::HeadReport (report.hpp:12-23) of one (batch, q head)."""
+
+    _fields_ = [("head", i64), ("tau", C.c_double), ("sparsity", C.c_double), ("err", C.c_double),
+                ("computed_blocks", i64), ("skipped_blocks", i64), ("total_blocks", i64),
+                ("coverage_min", i64), ("coverage_max", i64), ("coverage_mean", C.c_double)]
+
+
+class StageTiming(C.Structure):
+    _fields_ = [("quantization_ms", C.c_double), ("selection_ms", C.c_double),
+                ("computation_ms", C.c_double), ("dense_ms", C.c_double)]
+
+
+class SweepRow(C.Structure):
+    _fields_ = [("tau", C.c_double), ("sparsity", C.c_double), ("err", C.c_double)]
+
+
+class CalibrationSettings(C.Structure):
+    """sale::CalibrationSettings (calibrate.hpp:56-68) minus the geometry."""
+
+    _fields_ = [("theta", C.c_double), ("tau0", C.c_double), ("max_halvings", i64)]
+
+
+class HeadCalibration(C.Structure):
+    _fields_ = [("layer", i64), ("head", i64), ("tau", C.c_double), ("flag", C.c_int32),
+                ("halvings", i64)]
+
+
 _ERRORS = {1: ValueError, 2: ArithmeticError, 3: IndexError, 4: RuntimeError,
-           5: NotImplementedError}
+           5: NotImplementedError, 6: TensorFileError, 7: OSError}
 
 _lib = None
 
@@ -86,6 +125,21 @@ def load_library() -> C.CDLL:
         "sale_b200_workload_gqa_shard_bf16": (C.c_int, [C.c_int, C.c_uint64, P(Shape), i64, vp,
                                                         vp, vp, C.c_int]),
         "sale_b200_set_timing": (C.c_int, [vp, C.c_int]),
+        "sale_b200_l1_error": (C.c_int, [vp, vp, vp, P(Shape), vp]),
+        "sale_b200_run_pipeline": (C.c_int, [vp, vp, vp, vp, P(Shape), P(C.c_double),
+                                             P(SelectionConfig), C.c_int, P(HeadReport),
+                                             P(StageTiming)]),
+        "sale_b200_sweep_thresholds": (C.c_int, [vp, vp, vp, vp, P(Shape), P(C.c_double), i64,
+                                                 P(SelectionConfig), P(SweepRow)]),
+        "sale_b200_calibrate": (C.c_int, [vp, P(vp), P(vp), P(vp), i64, P(Shape),
+                                          P(CalibrationSettings), P(SelectionConfig),
+                                          P(HeadCalibration)]),
+        "sale_b200_tensor_file_info": (C.c_int, [C.c_char_p, vp, vp, vp, vp]),
+        "sale_b200_tensor_file_read_bf16": (C.c_int, [C.c_char_p, vp, vp, vp]),
+        "sale_b200_tensor_file_write": (C.c_int, [C.c_char_p, vp, vp, vp, C.c_uint32, C.c_uint32,
+                                                  C.c_uint32, C.c_uint32]),
+        "sale_b200_mask_dump_write": (C.c_int, [C.c_char_p, vp, i64, i64, i64, vp]),
+        "sale_b200_mask_dump_read": (C.c_int, [C.c_char_p, vp, vp, vp, vp, vp, vp]),
         "sale_b200_stage_times": (C.c_int, [vp, P(C.c_float)]),
     }
     for name, (res, args) in sig.items():
@@ -316,6 +370,166 @@ def prefill_host(q, k, v, taus, out, head_dim=128, config=None):
                                               taus.ctypes.data_as(C.POINTER(C.c_double)),
                                               C.byref(cfg), ptr(out)))
     return out
+
+
+# --------------------------------------------------- orchestration (device)
+
+TIMING_LABEL = "B200 (sm_100a)"
+
+
+def l1_error(reference, approx, head_dim=128):
+    """l1_error (calibrate.hpp:20-29) per (batch, q head) of two bf16 outputs
+    [B, N, Hq, 128]: mean over tokens of the L1 distance. -> float64 [B, Hq]."""
+    ctx = context()
+    B, N, H, _ = reference.shape
+    s = Shape(B, N, H, H, head_dim)
+    out = np.empty((B, H), np.float64)
+    ctx._check(ctx.lib.sale_b200_l1_error(ctx.handle, _ptr(reference), _ptr(approx), C.byref(s),
+                                          out.ctypes.data))
+    return out
+
+
+def run_pipeline(q, k, v, taus, config=None, dense_mask=False, head_dim=128):
+    """run_pipeline (runner.hpp:37-108) for every (batch, q head) of device
+    tensors; returns the RunReport as report.hpp:51-87's to_json dict (head
+    index b*Hq+h; "timing" holds device-event stage times of the whole batch,
+    label TIMING_LABEL)."""
+    ctx = context()
+    s = _shape_of(q, k, head_dim)
+    taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (s.q_heads,)))
+    cfg = config if config is not None else default_config()
+    reps = (HeadReport * (s.batch * s.q_heads))()
+    tm = StageTiming()
+    ctx._check(ctx.lib.sale_b200_run_pipeline(ctx.handle, _ptr(q), _ptr(k), _ptr(v), C.byref(s),
+                                              taus.ctypes.data_as(C.POINTER(C.c_double)),
+                                              C.byref(cfg), int(bool(dense_mask)), reps,
+                                              C.byref(tm)))
+    heads = [{"head": r.head, "tau": r.tau, "sparsity": r.sparsity, "err": r.err,
+              "computed_blocks": r.computed_blocks, "skipped_blocks": r.skipped_blocks,
+              "total_blocks": r.total_blocks,
+              "coverage": {"min": r.coverage_min, "max": r.coverage_max,
+                           "mean": r.coverage_mean}} for r in reps]
+    t = {"label": TIMING_LABEL, "quantization_ms": tm.quantization_ms,
+         "selection_ms": tm.selection_ms, "computation_ms": tm.computation_ms,
+         "dense_ms": tm.dense_ms}
+    t["overhead_ratio"] = ((t["quantization_ms"] + t["selection_ms"]) / t["dense_ms"]
+                           if t["dense_ms"] > 0 else 0.0)
+    t["computation_speedup"] = t["dense_ms"] / t["computation_ms"] if t["computation_ms"] > 0 else 0.0
+    return {"version": 1, "kind": "run_report", "tokens": s.tokens, "head_dim": s.head_dim,
+            "heads": s.batch * s.q_heads,
+            "selection": {"sink_tokens": cfg.sink_tokens, "local_tokens_min": cfg.local_tokens_min,
+                          "segment_size": cfg.segment_size, "block_q": cfg.block_q,
+                          "block_k": cfg.block_k},
+            "head_reports": heads, "timing": t}
+
+
+def strip_timing(report: dict) -> dict:
+    """report.hpp:89-92: the report without wall-clock data, for diffs."""
+    return {k: v for k, v in report.items() if k != "timing"}
+
+
+def sweep_thresholds(q, k, v, taus, config=None, head_dim=128):
+    """sweep_thresholds (runner.hpp:119-165): rows [{tau, sparsity (mean over
+    heads), err (max over heads)}] in the given order."""
+    ctx = context()
+    s = _shape_of(q, k, head_dim)
+    taus = np.ascontiguousarray(np.asarray(taus, np.float64).ravel())
+    rows = (SweepRow * max(1, len(taus)))()
+    cfg = config if config is not None else default_config()
+    ctx._check(ctx.lib.sale_b200_sweep_thresholds(ctx.handle, _ptr(q), _ptr(k), _ptr(v), C.byref(s),
+                                                  taus.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  len(taus), C.byref(cfg), rows))
+    return [{"tau": r.tau, "sparsity": r.sparsity, "err": r.err} for r in rows[:len(taus)]]
+
+
+def calibrate_model(samples, theta=0.4, tau0=0.008, max_halvings=30, config=None, head_dim=128,
+                    sample_names=None):
+    """calibrate_model (calibrate.hpp:149-175): samples = [(q, k, v), ...]
+    device tensors [1, N, Hq, 128] / [1, N, Hkv, 128]; every q head runs the
+    greedy halving ladder on the device. Returns the CalibrationProfile as
+    profile_io.hpp:16-30's JSON dict."""
+    ctx = context()
+    if not samples:
+        raise ValueError("calibrate_model: no samples")
+    s = _shape_of(samples[0][0], samples[0][1], head_dim)
+    n = len(samples)
+    arr = lambda i: (vp * n)(*[C.c_void_p(x[i].data_ptr()) for x in samples])
+    st = CalibrationSettings(theta, tau0, max_halvings)
+    out = (HeadCalibration * s.q_heads)()
+    cfg = config if config is not None else default_config()
+    ctx._check(ctx.lib.sale_b200_calibrate(ctx.handle, arr(0), arr(1), arr(2), n, C.byref(s),
+                                           C.byref(st), C.byref(cfg), out))
+    return {"version": 1, "tau0": tau0, "theta": theta,
+            "samples": list(sample_names or []),
+            "heads": [{"layer": h.layer, "head": h.head, "tau": h.tau,
+                       "flag": "converged" if h.flag == 0 else "floor-reached",
+                       "halvings": h.halvings} for h in out]}
+
+
+# ------------------------------------------------------------ file formats
+
+def _file_check(status):
+    if status:
+        lib = load_library()
+        raise _ERRORS.get(status, RuntimeError)((lib.sale_b200_last_error(None) or b"").decode())
+
+
+def read_tensor_file(path):
+    """read_tensor_file (tensor_file.hpp:98-158) into this path's layout:
+    (q, k, v) bf16 bit patterns uint16 [1, N, H, 128] (MHA) and the head dim."""
+    lib = load_library()
+    h, n, d, t = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    _file_check(lib.sale_b200_tensor_file_info(path.encode(), C.byref(h), C.byref(n), C.byref(d),
+                                               C.byref(t)))
+    q, k, v = (np.empty((1, n.value, h.value, HEAD_PITCH), np.uint16) for _ in range(3))
+    _file_check(lib.sale_b200_tensor_file_read_bf16(path.encode(), q.ctypes.data, k.ctypes.data,
+                                                    v.ctypes.data))
+    return q, k, v, d.value
+
+
+def write_tensor_file(path, q, k, v, head_dim, dtype="f32"):
+    """write_tensor_file (tensor_file.hpp:69-96) from bf16 bit patterns
+    [1, N, H, 128]; dtype "f32" (the reference's tag 1) or "bf16" (tag 2)."""
+    lib = load_library()
+    _, n, h, _ = q.shape
+    a = lambda x: np.ascontiguousarray(x, np.uint16)
+    q, k, v = a(q), a(k), a(v)
+    _file_check(lib.sale_b200_tensor_file_write(path.encode(), q.ctypes.data, k.ctypes.data,
+                                                v.ctypes.data, h, n, head_dim,
+                                                {"f32": 1, "bf16": 2}[dtype]))
+
+
+def write_mask_dump(path, mask_words, tokens, taus):
+    """write_mask_dump (mask_io.hpp:28-69) from packed mask words
+    [B, Hq, nq, W] (host numpy or device tensor): one record per (b, h)."""
+    lib = load_library()
+    words = mask_words.cpu().numpy() if hasattr(mask_words, "cpu") else np.asarray(mask_words)
+    words = np.ascontiguousarray(words.view(np.uint32))
+    B, H = words.shape[:2]
+    t = np.asarray(taus, np.float32).ravel()
+    t = np.ascontiguousarray(np.resize(t, B * H) if t.size in (1, H) else t)
+    if t.size != B * H:
+        raise ValueError("write_mask_dump: taus must be scalar, per head or per record")
+    _file_check(lib.sale_b200_mask_dump_write(path.encode(), words.ctypes.data, B, H, tokens,
+                                              t.ctypes.data))
+
+
+def read_mask_dump(path):
+    """read_mask_dump (mask_io.hpp:71-125) -> (packed words [R, nq, W] uint32,
+    head indices [R], taus float32 [R])."""
+    lib = load_library()
+    r, nq, nk = C.c_int64(), C.c_int64(), C.c_int64()
+    _file_check(lib.sale_b200_mask_dump_read(path.encode(), C.byref(r), C.byref(nq), C.byref(nk),
+                                             None, None, None))
+    if r.value == 0:
+        return np.zeros((0, 0, 0), np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.float32)
+    W = (nk.value + 31) // 32
+    words = np.zeros((r.value, nq.value, W), np.uint32)
+    heads = np.zeros(r.value, np.uint32)
+    taus = np.zeros(r.value, np.float32)
+    _file_check(lib.sale_b200_mask_dump_read(path.encode(), None, None, None, words.ctypes.data,
+                                             heads.ctypes.data, taus.ctypes.data))
+    return words, heads, taus
 
 
 # ------------------------------------------------------------- multi-GPU
