@@ -14,6 +14,18 @@
 //   sale::b200::full_attention           attention.hpp:18
 //   sale::b200::flop_accounting          sparse_attention.hpp:101
 //
+// and, when the reference's orchestration headers are included first
+// (sale/runner.hpp with sale/report.hpp, sale/calibrate.hpp, sale/mask_io.hpp)
+// and SALE_B200_WITH_RUNNER is defined, the layer above the stages with every
+// head in the same device launches:
+//
+//   sale::b200::run_pipeline             runner.hpp:37
+//   sale::b200::sweep_thresholds         runner.hpp:119
+//   sale::b200::calibrate_head           calibrate.hpp:121
+//   sale::b200::calibrate_model          calibrate.hpp:149
+//   sale::b200::read_tensor_file         tensor_file.hpp:98
+//   sale::b200::write_mask_dump          mask_io.hpp:28
+//
 // A call site switches with `using sale::b200::selection_pass;` (or a
 // namespace alias), see INTEGRATION.md.
 //
@@ -31,6 +43,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -294,6 +307,226 @@ inline FlopCounts flop_accounting(const BlockMask &mask, const BlockGrid &grid) 
     f.total_blocks = static_cast<std::size_t>(h[2]);
     return f;
 }
+
+// ------------------------------------------------ orchestration (optional)
+// Compiled when the reference's runner / calibration / format headers were
+// included before this one (their include guards are `#pragma once`, so the
+// checks use a type the header defines through a feature macro of ours).
+#if defined(SALE_B200_WITH_RUNNER)
+namespace detail {
+// heads [h][n][d] fp32 -> device bf16 [1][n][h][128] (an MHA shape)
+inline void upload_heads(std::span<const HeadInput> heads, int which, const Buf &dst) {
+    const std::size_t h = heads.size(), n = heads.front().seq_len(), d = heads.front().head_dim();
+    std::vector<uint16_t> buf(n * h * 128, 0);
+    for (std::size_t i = 0; i < h; ++i) {
+        const DenseMatrix &m = which == 0 ? heads[i].query : which == 1 ? heads[i].key : heads[i].value;
+        for (std::size_t r = 0; r < n; ++r)
+            for (std::size_t c = 0; c < d; ++c) buf[(r * h + i) * 128 + c] = to_bf16(m(r, c));
+    }
+    check(sale_b200_copy_to_device(ctx(), dst.p, buf.data(), buf.size() * 2));
+}
+inline void check_heads(std::span<const HeadInput> heads, const char *who) {
+    if (heads.empty()) throw std::invalid_argument(std::string(who) + ": no heads");
+    for (const HeadInput &h : heads) {
+        h.validate();
+        if (h.seq_len() != heads.front().seq_len() || h.head_dim() != heads.front().head_dim())
+            throw std::invalid_argument(std::string(who) + ": heads disagree on shape");
+    }
+    check_dim(heads.front().head_dim());
+}
+inline sale_b200_selection_config config_of(const SelectionConfig &c) {
+    return {static_cast<int64_t>(c.sink_tokens), static_cast<int64_t>(c.local_tokens_min),
+            static_cast<int64_t>(c.segment_size), static_cast<int64_t>(c.block_q),
+            static_cast<int64_t>(c.block_k)};
+}
+struct DeviceHeads {
+    sale_b200_shape shape;
+    std::unique_ptr<Buf> q, k, v;
+    explicit DeviceHeads(std::span<const HeadInput> heads) {
+        const std::size_t h = heads.size(), n = heads.front().seq_len();
+        shape = {1, static_cast<int64_t>(n), static_cast<int64_t>(h), static_cast<int64_t>(h),
+                 static_cast<int64_t>(heads.front().head_dim())};
+        q = std::make_unique<Buf>(n * h * 256);
+        k = std::make_unique<Buf>(n * h * 256);
+        v = std::make_unique<Buf>(n * h * 256);
+        upload_heads(heads, 0, *q);
+        upload_heads(heads, 1, *k);
+        upload_heads(heads, 2, *v);
+    }
+};
+} // namespace detail
+
+// runner.hpp:37 — every head in the same launches; RunReport fields as the
+// reference's, timing = device-event stage times of the whole call (the
+// reference sums per-head thread times).
+inline RunReport run_pipeline(std::span<const HeadInput> heads, std::span<const double> taus,
+                              const SelectionConfig &base, const RunOptions &options) {
+    detail::check_heads(heads, "run_pipeline");
+    if (taus.size() != heads.size()) throw std::invalid_argument("run_pipeline: tau count != head count");
+    detail::DeviceHeads dh(heads);
+    const sale_b200_selection_config cfg = detail::config_of(base);
+    std::vector<sale_b200_head_report> reps(heads.size());
+    sale_b200_stage_timing t{};
+    detail::check(sale_b200_run_pipeline(detail::ctx(), dh.q->p, dh.k->p, dh.v->p, &dh.shape,
+                                         taus.data(), &cfg, options.dense_mask ? 1 : 0, reps.data(), &t));
+    RunReport report;
+    report.tokens = heads.front().seq_len();
+    report.head_dim = heads.front().head_dim();
+    report.heads = heads.size();
+    report.selection = base;
+    report.head_reports.resize(heads.size());
+    for (std::size_t h = 0; h < heads.size(); ++h) {
+        HeadReport &r = report.head_reports[h];
+        r.head = h;
+        r.tau = reps[h].tau;
+        r.sparsity = reps[h].sparsity;
+        r.err = reps[h].err;
+        r.computed_blocks = static_cast<std::size_t>(reps[h].computed_blocks);
+        r.skipped_blocks = static_cast<std::size_t>(reps[h].skipped_blocks);
+        r.total_blocks = static_cast<std::size_t>(reps[h].total_blocks);
+        r.coverage_min = static_cast<std::size_t>(reps[h].coverage_min);
+        r.coverage_max = static_cast<std::size_t>(reps[h].coverage_max);
+        r.coverage_mean = reps[h].coverage_mean;
+    }
+    report.timing.quantization_ms = t.quantization_ms;
+    report.timing.selection_ms = t.selection_ms;
+    report.timing.computation_ms = t.computation_ms;
+    report.timing.dense_ms = t.dense_ms;
+    return report;
+}
+
+// runner.hpp:119
+inline std::vector<SweepRow> sweep_thresholds(std::span<const HeadInput> heads,
+                                              std::span<const double> taus,
+                                              const SelectionConfig &base, std::size_t = 1) {
+    detail::check_heads(heads, "sweep_thresholds");
+    if (taus.empty()) throw std::invalid_argument("sweep_thresholds: empty grid");
+    detail::DeviceHeads dh(heads);
+    const sale_b200_selection_config cfg = detail::config_of(base);
+    std::vector<sale_b200_sweep_row> rows(taus.size());
+    detail::check(sale_b200_sweep_thresholds(detail::ctx(), dh.q->p, dh.k->p, dh.v->p, &dh.shape,
+                                             taus.data(), static_cast<int64_t>(taus.size()), &cfg,
+                                             rows.data()));
+    std::vector<SweepRow> out(taus.size());
+    for (std::size_t t = 0; t < taus.size(); ++t) {
+        out[t].tau = rows[t].tau;
+        out[t].sparsity = rows[t].sparsity;
+        out[t].err = rows[t].err;
+    }
+    return out;
+}
+
+// calibrate.hpp:149 — samples[s][h]; every head's halving ladder runs in the
+// same device launches.
+inline CalibrationProfile calibrate_model(std::span<const std::vector<HeadInput>> samples,
+                                          const CalibrationSettings &settings, std::size_t = 1) {
+    if (samples.empty()) throw std::invalid_argument("calibrate_model: no samples");
+    const std::size_t head_count = samples.front().size();
+    if (head_count == 0) throw std::invalid_argument("calibrate_model: samples carry no heads");
+    for (const auto &s : samples)
+        if (s.size() != head_count)
+            throw std::invalid_argument("calibrate_model: inconsistent head count across samples");
+    settings.validate();
+    settings.selection.validate();
+    std::vector<std::unique_ptr<detail::DeviceHeads>> dev;
+    std::vector<const void *> qp, kp, vp;
+    for (const auto &s : samples) {
+        detail::check_heads(s, "calibrate_model");
+        dev.push_back(std::make_unique<detail::DeviceHeads>(s));
+        qp.push_back(dev.back()->q->p);
+        kp.push_back(dev.back()->k->p);
+        vp.push_back(dev.back()->v->p);
+    }
+    for (const auto &d : dev)
+        if (d->shape.tokens != dev.front()->shape.tokens || d->shape.head_dim != dev.front()->shape.head_dim)
+            detail::raise(SALE_B200_UNSUPPORTED, "calibration samples of different shapes");
+    const sale_b200_calibration_settings st{settings.theta, settings.tau0,
+                                            static_cast<int64_t>(settings.max_halvings)};
+    const sale_b200_selection_config cfg = detail::config_of(settings.selection);
+    std::vector<sale_b200_head_calibration> out(head_count);
+    detail::check(sale_b200_calibrate(detail::ctx(), qp.data(), kp.data(), vp.data(),
+                                      static_cast<int64_t>(samples.size()), &dev.front()->shape, &st,
+                                      &cfg, out.data()));
+    CalibrationProfile profile;
+    profile.tau0 = settings.tau0;
+    profile.theta = settings.theta;
+    profile.heads.resize(head_count);
+    for (std::size_t h = 0; h < head_count; ++h) {
+        HeadCalibration &c = profile.heads[h];
+        c.layer = 0;
+        c.head = h;
+        c.tau = out[h].tau;
+        c.flag = out[h].flag == 0 ? CalibrationFlag::Converged : CalibrationFlag::FloorReached;
+        c.halvings = static_cast<std::size_t>(out[h].halvings);
+    }
+    return profile;
+}
+
+// calibrate.hpp:121 — one head, many samples
+inline HeadCalibration calibrate_head(std::span<const HeadInput> samples,
+                                      const CalibrationSettings &settings) {
+    if (samples.empty()) throw std::invalid_argument("calibrate_head: no samples");
+    std::vector<std::vector<HeadInput>> per(samples.size());
+    for (std::size_t s = 0; s < samples.size(); ++s) per[s] = {samples[s]};
+    return b200::calibrate_model(std::span<const std::vector<HeadInput>>(per), settings).heads.front();
+}
+
+// tensor_file.hpp:98 — through libsale_b200's reader (values come back
+// bf16-rounded: this path computes on bf16); TensorFileError with the same
+// message and offset as the reference's.
+inline std::vector<HeadInput> read_tensor_file(const std::string &path) {
+    uint32_t heads = 0, tokens = 0, dim = 0, dtype = 0;
+    auto io = [](int st) {
+        if (st == SALE_B200_FORMAT_ERROR) {
+            std::string m = sale_b200_last_error(nullptr);
+            const auto at = m.rfind(" (offset ");
+            const std::uint64_t off = at == std::string::npos ? 0 : std::stoull(m.substr(at + 9));
+            throw TensorFileError(at == std::string::npos ? m : m.substr(0, at), off);
+        }
+        if (st == SALE_B200_IO_ERROR) throw std::runtime_error(sale_b200_last_error(nullptr));
+        if (st) detail::raise(st, sale_b200_last_error(nullptr));
+    };
+    io(sale_b200_tensor_file_info(path.c_str(), &heads, &tokens, &dim, &dtype));
+    std::vector<uint16_t> q(std::size_t(tokens) * heads * 128), k(q.size()), v(q.size());
+    io(sale_b200_tensor_file_read_bf16(path.c_str(), q.data(), k.data(), v.data()));
+    std::vector<HeadInput> out(heads);
+    for (uint32_t h = 0; h < heads; ++h)
+        for (int m = 0; m < 3; ++m) {
+            const std::vector<uint16_t> &src = m == 0 ? q : m == 1 ? k : v;
+            DenseMatrix &dst = m == 0 ? out[h].query : m == 1 ? out[h].key : out[h].value;
+            dst = DenseMatrix(tokens, dim);
+            for (uint32_t r = 0; r < tokens; ++r)
+                for (uint32_t c = 0; c < dim; ++c)
+                    dst(r, c) = detail::from_bf16(src[(std::size_t(r) * heads + h) * 128 + c]);
+        }
+    return out;
+}
+
+// mask_io.hpp:28 — records must share one default-geometry grid and carry head
+// indices 0, 1, ... in order (the layout libsale_b200 writes from packed masks).
+inline void write_mask_dump(const std::string &path, std::span<const MaskRecord> records) {
+    if (records.empty()) throw std::invalid_argument("write_mask_dump: no records");
+    const std::size_t nq = records.front().mask.query_blocks(), nk = records.front().mask.key_blocks();
+    const std::size_t tokens = 32 * nk; // any n with these block counts encodes the same grid
+    if ((tokens + 63) / 64 != nq)
+        detail::raise(SALE_B200_UNSUPPORTED, "mask grid is not a block_q 64 / block_k 32 grid");
+    std::vector<uint32_t> words;
+    std::vector<float> taus;
+    for (std::size_t r = 0; r < records.size(); ++r) {
+        const MaskRecord &rec = records[r];
+        if (rec.head != r || rec.mask.query_blocks() != nq || rec.mask.key_blocks() != nk)
+            detail::raise(SALE_B200_UNSUPPORTED, "records must be heads 0.. of one grid");
+        const std::vector<uint32_t> p = detail::pack(rec.mask);
+        words.insert(words.end(), p.begin(), p.end());
+        taus.push_back(rec.tau);
+    }
+    const int st = sale_b200_mask_dump_write(path.c_str(), words.data(), 1,
+                                             static_cast<int64_t>(records.size()),
+                                             static_cast<int64_t>(tokens), taus.data());
+    if (st == SALE_B200_IO_ERROR) throw std::runtime_error(sale_b200_last_error(nullptr));
+    if (st) detail::raise(st, sale_b200_last_error(nullptr));
+}
+#endif // SALE_B200_WITH_RUNNER
 
 } // namespace b200
 } // namespace sale

@@ -9,8 +9,16 @@
 #include <sale/selection.hpp>
 #include <sale/sparse_attention.hpp>
 #include <sale/workloads.hpp>
+#include <sale/calibrate.hpp>
+#include <sale/mask_io.hpp>
+#include <sale/runner.hpp>
+#include <sale/tensor_file.hpp>
 
+#define SALE_B200_WITH_RUNNER
 #include "sale_b200.hpp"
+
+#include <fstream>
+#include <iterator>
 
 #include <cmath>
 #include <cstdio>
@@ -127,6 +135,87 @@ int main() {
         BlockMask all(4, 8);
         all.set_all(true);
         CHECK_THROWS_AS(b200::block_sparse_attention(in, all, grid), std::invalid_argument);
+    }
+    // runner.hpp:37 run_pipeline / :119 sweep_thresholds (every head in one launch)
+    {
+        std::vector<HeadInput> heads;
+        for (std::size_t h = 0; h < 3; ++h) heads.push_back(sink_head(300 + h, 1024, 64));
+        const std::vector<double> taus = {0.004, 0.02, 0.001};
+        SelectionConfig base;
+        RunOptions opt;
+        opt.threads = 3;
+        const RunReport ref = run_pipeline(heads, taus, base, opt);
+        const RunReport got = b200::run_pipeline(heads, taus, base, opt);
+        CHECK(got.tokens == ref.tokens && got.heads == ref.heads && got.head_dim == ref.head_dim);
+        for (std::size_t h = 0; h < 3; ++h) {
+            const HeadReport &a = ref.head_reports[h], &b = got.head_reports[h];
+            CHECK(a.computed_blocks == b.computed_blocks && a.skipped_blocks == b.skipped_blocks &&
+                  a.total_blocks == b.total_blocks && a.sparsity == b.sparsity);
+            CHECK(a.coverage_min == b.coverage_min && a.coverage_max == b.coverage_max);
+            CHECK(std::fabs(a.coverage_mean - b.coverage_mean) < 1e-9);
+            CHECK(std::fabs(a.err - b.err) <= 0.03 * a.err + 2e-3);
+        }
+        CHECK(got.timing.dense_ms > 0.0 && got.timing.overhead_ratio() > 0.0);
+        const std::vector<double> grid = {0.002, 0.008, 0.032};
+        const auto rs = sweep_thresholds(heads, grid, base, 3);
+        const auto gs = b200::sweep_thresholds(heads, grid, base);
+        for (std::size_t t = 0; t < grid.size(); ++t) {
+            CHECK(gs[t].tau == rs[t].tau);
+            CHECK(std::fabs(gs[t].sparsity - rs[t].sparsity) < 1e-15);
+            CHECK(std::fabs(gs[t].err - rs[t].err) <= 0.03 * rs[t].err + 2e-3);
+        }
+    }
+    // calibrate.hpp:121 calibrate_head — same rung as the reference
+    {
+        std::vector<HeadInput> samples = {sink_head(7, 1024, 64), sink_head(8, 1024, 64)};
+        CalibrationSettings st;
+        st.max_halvings = 12;
+        const HeadCalibration ref = calibrate_head(samples, st);
+        const HeadCalibration got = b200::calibrate_head(samples, st);
+        CHECK(got.tau == ref.tau && got.halvings == ref.halvings && got.flag == ref.flag);
+        st.theta = -1.0;
+        CHECK_THROWS_AS(b200::calibrate_head(samples, st), std::invalid_argument);
+    }
+    // tensor_file.hpp:98 / mask_io.hpp:28 — interchange with the reference
+    {
+        std::vector<HeadInput> heads = {sink_head(41, 200, 48), sink_head(42, 200, 48)};
+        const std::string tns = "/tmp/sale_b200_shim.tns", msk_ref = "/tmp/sale_b200_ref.mask",
+                          msk_got = "/tmp/sale_b200_got.mask";
+        write_tensor_file(tns, heads);
+        const std::vector<HeadInput> back = b200::read_tensor_file(tns);
+        CHECK(back.size() == 2 && back[1].value.data() == heads[1].value.data());
+        {
+            std::ofstream bad(tns, std::ios::binary | std::ios::trunc);
+            bad << "SALETNSR";
+        }
+        bool matched = false;
+        try {
+            (void)read_tensor_file(tns);
+        } catch (const TensorFileError &ref_e) {
+            try {
+                (void)b200::read_tensor_file(tns);
+            } catch (const TensorFileError &e) {
+                matched = std::string(e.what()) == ref_e.what() && e.offset() == ref_e.offset();
+            }
+        }
+        CHECK(matched);
+        std::vector<MaskRecord> recs;
+        for (std::size_t h = 0; h < 2; ++h) {
+            MaskRecord r;
+            r.head = static_cast<std::uint32_t>(h);
+            r.tau = 0.004f * static_cast<float>(h + 1);
+            const BlockGrid grid(200, 64, 32);
+            SelectionConfig cfg;
+            cfg.tau = r.tau;
+            r.mask = selection_pass(heads[h], quantize_per_token(heads[h].query),
+                                    quantize_per_key_block(heads[h].key, grid), cfg);
+            recs.push_back(r);
+        }
+        write_mask_dump(msk_ref, recs);
+        b200::write_mask_dump(msk_got, recs);
+        std::ifstream a(msk_ref, std::ios::binary), b(msk_got, std::ios::binary);
+        const std::string ra((std::istreambuf_iterator<char>(a)), {}), rb((std::istreambuf_iterator<char>(b)), {});
+        CHECK(!ra.empty() && ra == rb);
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL OK", failures);
     return failures ? 1 : 0;
