@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const uint32_t *__restrict__ mask,
                         __nv_bfloat16 *__restrict__ out, int32_t *__restrict__ coverage,
-                        int64_t tokens, int hq, int hkv, float scale_log2) {
+                        int64_t tokens, int hq, int hkv, float scale_log2, int64_t i_lo,
+                        int64_t ni) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     AttnSmem &sm = *reinterpret_cast<AttnSmem *>(smem_raw + smem_pad_1k(smem_raw));
     const int warp = threadIdx.x >> 5;
@@ -290,8 +291,9 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
     const int group = hq / hkv;
     const int npairs = (group + 1) / 2;
     const int p = static_cast<int>(blockIdx.x % npairs);
-    const int64_t i = nq - 1 - static_cast<int64_t>((blockIdx.x / npairs) % nq);
-    const int bg = static_cast<int>(blockIdx.x / (npairs * nq));
+    // query blocks [i_lo, i_lo + ni): a token-range slice (chunked host pipeline)
+    const int64_t i = i_lo + ni - 1 - static_cast<int64_t>((blockIdx.x / npairs) % ni);
+    const int bg = static_cast<int>(blockIdx.x / (npairs * ni));
     const int g = bg % hkv;
     const int b = bg / hkv;
     const int hA = g * group + 2 * p;
@@ -575,7 +577,7 @@ size_t attention_smem_bytes() { return sizeof(AttnSmem) + 1024; }
 cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
                                     const uint32_t *mask, void *out, int32_t *coverage,
                                     int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
-                                    cudaStream_t stream) {
+                                    cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     if (nq / 2 + 3 > kMaxTiles) return cudaErrorInvalidValue;
     static bool configured = false;
@@ -588,10 +590,12 @@ cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, cons
         configured = true;
     }
     const int npairs = (hq / hkv + 1) / 2;
-    const int64_t grid = batch * hkv * npairs * nq;
+    if (i_hi < 0 || i_hi > nq) i_hi = nq;
+    if (i_hi <= i_lo) return cudaSuccess;
+    const int64_t grid = batch * hkv * npairs * (i_hi - i_lo);
     sparse_attention_kernel<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
         static_cast<const __nv_bfloat16 *>(q), tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out),
-        coverage, tokens, hq, hkv, scale_log2);
+        coverage, tokens, hq, hkv, scale_log2, i_lo, i_hi - i_lo);
     return cudaGetLastError();
 }
 

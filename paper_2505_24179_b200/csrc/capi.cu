@@ -37,6 +37,13 @@ struct sale_b200_ctx {
     uint8_t *io = nullptr;
     size_t io_bytes = 0;
     cudaStream_t io_stream = nullptr;
+    // chunked host pipeline (sale_b200_prefill_host): compute and D2H streams,
+    // per-chunk estimator units grouped by chunk
+    cudaStream_t comp_stream = nullptr, out_stream = nullptr;
+    EstUnit *d_cunits = nullptr;
+    size_t cunits_bytes = 0;
+    std::vector<int64_t> cunit_key;
+    std::vector<int64_t> cunit_off;
     // optional per-stage event timing of sale_b200_prefill
     bool timing = false;
     cudaEvent_t ev[6] = {};
@@ -290,6 +297,65 @@ int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void 
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Query-block boundaries of the chunked host pipeline: chunk c = query blocks
+// [b_c, b_{c+1}); inner boundaries are odd so that every estimator tile
+// (query blocks 2m+1, 2m+2) lies inside one chunk. Equal token spans.
+std::vector<int64_t> chunk_bounds(int64_t nq, int chunks) {
+    std::vector<int64_t> b(1, 0);
+    for (int c = 1; c < chunks; ++c) {
+        int64_t x = (nq * c) / chunks;
+        x |= 1; // odd
+        if (x > b.back() && x < nq) b.push_back(x);
+    }
+    b.push_back(nq);
+    return b;
+}
+
+// Estimator units grouped by chunk (tile m belongs to the chunk holding query
+// block 2m+1), each group ordered like the global table.
+int ensure_chunk_units(sale_b200_ctx *ctx, int64_t tokens, const std::vector<int64_t> &bounds,
+                       cudaStream_t stream) {
+    std::vector<int64_t> key(bounds);
+    key.push_back(tokens);
+    if (key == ctx->cunit_key) return SALE_B200_OK;
+    const int64_t nq = cdiv(tokens, kBlockQ);
+    const size_t nch = bounds.size() - 1;
+    std::vector<std::vector<EstUnit>> per(nch);
+    for (int64_t m = 2; 2 * m + 1 <= nq - 1; ++m) {
+        const int64_t f = m - 1;
+        size_t c = 0;
+        while (c + 1 < nch && bounds[c + 1] <= 2 * m + 1) ++c;
+        for (int64_t cc = 0; cc * kSegPerUnitHost < f; ++cc)
+            per[c].push_back({static_cast<int>(m), static_cast<int>(cc),
+                              static_cast<int>(std::min<int64_t>(kSegPerUnitHost, f - cc * kSegPerUnitHost))});
+    }
+    std::vector<EstUnit> flat;
+    ctx->cunit_off.assign(1, 0);
+    for (auto &v : per) {
+        std::stable_sort(v.begin(), v.end(), [](const EstUnit &a, const EstUnit &b) {
+            if (a.nseg != b.nseg) return a.nseg > b.nseg;
+            if (a.c != b.c) return a.c < b.c;
+            return a.m < b.m;
+        });
+        flat.insert(flat.end(), v.begin(), v.end());
+        ctx->cunit_off.push_back(static_cast<int64_t>(flat.size()));
+    }
+    const size_t bytes = sizeof(EstUnit) * std::max<size_t>(flat.size(), 1);
+    if (bytes > ctx->cunits_bytes) {
+        if (ctx->d_cunits) cudaFree(ctx->d_cunits);
+        ctx->d_cunits = nullptr;
+        ctx->cunits_bytes = 0;
+        SALE_CUDA(ctx, cudaMalloc(&ctx->d_cunits, bytes));
+        ctx->cunits_bytes = bytes;
+    }
+    if (!flat.empty())
+        SALE_CUDA(ctx, cudaMemcpyAsync(ctx->d_cunits, flat.data(), sizeof(EstUnit) * flat.size(),
+                                       cudaMemcpyHostToDevice, stream));
+    SALE_CUDA(ctx, cudaStreamSynchronize(stream));
+    ctx->cunit_key = key;
+    return SALE_B200_OK;
+}
+
 } // namespace
 
 namespace sale_b200 {
@@ -414,6 +480,9 @@ void sale_b200_ctx_destroy(sale_b200_ctx *ctx) {
     if (ctx->d_units) cudaFree(ctx->d_units);
     if (ctx->io) cudaFree(ctx->io);
     if (ctx->io_stream) cudaStreamDestroy(ctx->io_stream);
+    if (ctx->comp_stream) cudaStreamDestroy(ctx->comp_stream);
+    if (ctx->out_stream) cudaStreamDestroy(ctx->out_stream);
+    if (ctx->d_cunits) cudaFree(ctx->d_cunits);
     delete ctx;
 }
 
@@ -532,35 +601,90 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
                            const uint16_t *v, const sale_b200_shape *shape, const double *taus,
                            const sale_b200_selection_config *cfg, uint16_t *out) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
     int st;
-    {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        if ((st = check_shape(ctx, shape))) return st;
-        if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
-        const size_t qb = align256(2 * shape->batch * shape->tokens * shape->q_heads * kHeadDim);
-        const size_t kb = align256(2 * shape->batch * shape->tokens * shape->kv_heads * kHeadDim);
-        const size_t need = 2 * qb + 2 * kb;
-        if (need > ctx->io_bytes) {
-            if (ctx->io) cudaFree(ctx->io);
-            ctx->io = nullptr;
-            ctx->io_bytes = 0;
-            SALE_CUDA(ctx, cudaMalloc(&ctx->io, need));
-            ctx->io_bytes = need;
-        }
-        if (!ctx->io_stream)
-            SALE_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->io_stream, cudaStreamNonBlocking));
+    if ((st = check_shape(ctx, shape))) return st;
+    if ((st = check_config(ctx, cfg))) return st;
+    if ((st = check_taus(ctx, taus, shape->q_heads))) return st;
+    if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    const sale_b200_shape s = *shape;
+    const int64_t B = s.batch, N = s.tokens, Hq = s.q_heads, Hkv = s.kv_heads;
+    const size_t qbytes = 2 * B * N * Hq * kHeadDim, kbytes = 2 * B * N * Hkv * kHeadDim;
+    const size_t need = 2 * align256(qbytes) + 2 * align256(kbytes);
+    if (need > ctx->io_bytes) {
+        if (ctx->io) cudaFree(ctx->io);
+        ctx->io = nullptr;
+        ctx->io_bytes = 0;
+        SALE_CUDA(ctx, cudaMalloc(&ctx->io, need));
+        ctx->io_bytes = need;
     }
-    const size_t qbytes = 2 * shape->batch * shape->tokens * shape->q_heads * kHeadDim;
-    const size_t kbytes = 2 * shape->batch * shape->tokens * shape->kv_heads * kHeadDim;
+    for (cudaStream_t *p : {&ctx->io_stream, &ctx->comp_stream, &ctx->out_stream})
+        if (!*p) SALE_CUDA(ctx, cudaStreamCreateWithFlags(p, cudaStreamNonBlocking));
     uint8_t *dq = ctx->io, *dk = dq + align256(qbytes), *dv = dk + align256(kbytes),
             *dout = dv + align256(kbytes);
-    cudaStream_t s = ctx->io_stream;
-    SALE_CUDA(ctx, cudaMemcpyAsync(dq, q, qbytes, cudaMemcpyHostToDevice, s));
-    SALE_CUDA(ctx, cudaMemcpyAsync(dk, k, kbytes, cudaMemcpyHostToDevice, s));
-    SALE_CUDA(ctx, cudaMemcpyAsync(dv, v, kbytes, cudaMemcpyHostToDevice, s));
-    if ((st = sale_b200_prefill(ctx, dq, dk, dv, shape, taus, cfg, dout, nullptr, s))) return st;
-    SALE_CUDA(ctx, cudaMemcpyAsync(out, dout, qbytes, cudaMemcpyDeviceToHost, s));
-    SALE_CUDA(ctx, cudaStreamSynchronize(s));
+    cudaStream_t s_in = ctx->io_stream, s_comp = ctx->comp_stream, s_out = ctx->out_stream;
+    // The prefill in token chunks, three streams: the H2D copy of chunk c+1 and
+    // the D2H copy of chunk c-1 run under chunk c's kernels. Every stage only
+    // reads data of its own and earlier chunks (causal), so the result is
+    // bit-identical to the one-shot sale_b200_prefill.
+    const int64_t nq = cdiv(N, kBlockQ);
+    const int chunks = N >= 16384 ? 8 : (N >= 2048 ? 4 : 1);
+    const std::vector<int64_t> bounds = chunk_bounds(nq, chunks);
+    const size_t nch = bounds.size() - 1;
+    Workspace w;
+    if ((st = ensure_workspace(ctx, s, &w))) return st;
+    if ((st = upload_taus(ctx, taus, Hq, s_comp))) return st;
+    if ((st = ensure_chunk_units(ctx, N, bounds, s_comp))) return st;
+    CUtensorMap tm_qc, tm_kc, tk, tv;
+    if ((st = make_map(ctx, &tm_qc, w.q_codes, false, B, N, Hq, 128, 128))) return st;
+    if ((st = make_map(ctx, &tm_kc, w.k_codes, false, B, N, Hkv, 128, 128))) return st;
+    if ((st = make_map(ctx, &tk, dk, true, B, N, Hkv, 64, 128))) return st;
+    if ((st = make_map(ctx, &tv, dv, true, B, N, Hkv, 64, 128))) return st;
+    const float isd = inv_sqrt_dim(s.head_dim);
+    const float scale_log2 = isd * 1.4426950408889634f;
+    std::vector<cudaEvent_t> ev(2 * nch);
+    for (auto &e : ev) SALE_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EvFree {
+        std::vector<cudaEvent_t> &e;
+        ~EvFree() {
+            for (auto x : e) cudaEventDestroy(x);
+        }
+    } ev_free{ev};
+    auto copy_rows = [&](void *dst, const void *src, int64_t heads, int64_t t0, int64_t t1,
+                         cudaMemcpyKind kind, cudaStream_t st_) -> cudaError_t {
+        const size_t row = static_cast<size_t>(heads) * kHeadDim * 2; // bytes per token
+        const size_t off = static_cast<size_t>(t0) * row, pitch = static_cast<size_t>(N) * row;
+        return cudaMemcpy2DAsync(static_cast<uint8_t *>(dst) + off, pitch,
+                                 static_cast<const uint8_t *>(src) + off, pitch,
+                                 static_cast<size_t>(t1 - t0) * row, static_cast<size_t>(B), kind, st_);
+    };
+    for (size_t c = 0; c < nch; ++c) {
+        const int64_t i0 = bounds[c], i1 = bounds[c + 1];
+        const int64_t t0 = i0 * kBlockQ, t1 = std::min<int64_t>(i1 * kBlockQ, N);
+        SALE_CUDA(ctx, copy_rows(dq, q, Hq, t0, t1, cudaMemcpyHostToDevice, s_in));
+        SALE_CUDA(ctx, copy_rows(dk, k, Hkv, t0, t1, cudaMemcpyHostToDevice, s_in));
+        SALE_CUDA(ctx, copy_rows(dv, v, Hkv, t0, t1, cudaMemcpyHostToDevice, s_in));
+        SALE_CUDA(ctx, cudaEventRecord(ev[2 * c], s_in));
+        SALE_CUDA(ctx, cudaStreamWaitEvent(s_comp, ev[2 * c], 0));
+        SALE_CUDA(ctx, launch_quantize_qk(dq, dk, w.q_codes, w.q_scales, w.k_codes, w.k_scales, B, N,
+                                          Hq, Hkv, s_comp, t0, t1));
+        SALE_CUDA(ctx, launch_base_mask(w.mask, B, Hq, N, s_comp, i0, i1));
+        SALE_CUDA(ctx, launch_sink_local_stats(dq, dk, B, N, Hq, Hkv, isd, ctx->d_taus, w.thresh,
+                                               nullptr, nullptr, nullptr, s_comp, i0, i1));
+        const int64_t u0 = ctx->cunit_off[c], u1 = ctx->cunit_off[c + 1];
+        if (u1 > u0)
+            SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_cunits + u0, u1 - u0, w.q_scales,
+                                           w.k_scales, w.thresh, w.mask, B, N, static_cast<int>(Hq),
+                                           static_cast<int>(Hkv), isd, nullptr, s_comp));
+        SALE_CUDA(ctx, launch_sparse_attention(dq, tk, tv, w.mask, dout, nullptr, B, N,
+                                               static_cast<int>(Hq), static_cast<int>(Hkv),
+                                               scale_log2, s_comp, i0, i1));
+        SALE_CUDA(ctx, cudaEventRecord(ev[2 * c + 1], s_comp));
+        SALE_CUDA(ctx, cudaStreamWaitEvent(s_out, ev[2 * c + 1], 0));
+        SALE_CUDA(ctx, copy_rows(out, dout, Hq, t0, t1, cudaMemcpyDeviceToHost, s_out));
+    }
+    SALE_CUDA(ctx, cudaStreamSynchronize(s_out));
+    SALE_CUDA(ctx, cudaStreamSynchronize(s_comp));
     return SALE_B200_OK;
 }
 

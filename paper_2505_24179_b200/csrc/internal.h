@@ -25,15 +25,16 @@ constexpr int kSegPerUnitHost = 64;
 
 cudaError_t launch_quantize_qk(const void *q, const void *k, int8_t *q_codes, float *q_scales,
                                int8_t *k_codes, float *k_scales, int64_t batch, int64_t tokens,
-                               int64_t hq, int64_t hkv, cudaStream_t stream);
+                               int64_t hq, int64_t hkv, cudaStream_t stream, int64_t t_lo = 0,
+                               int64_t t_hi = -1);
 
 cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch, int64_t tokens,
                                     int64_t hq, int64_t hkv, float inv_sqrt_d, const double *taus,
                                     float *thresh, double *dbg_m, double *dbg_l, double *dbg_bound,
-                                    cudaStream_t stream);
+                                    cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1);
 
 cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
-                             cudaStream_t stream);
+                             cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1);
 
 size_t estimate_smem_bytes();
 cudaError_t estimate_profile(int enable, unsigned long long *out8);
@@ -49,7 +50,7 @@ cudaError_t attention_profile(int enable, unsigned long long *out16);
 cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
                                     const uint32_t *mask, void *out, int32_t *coverage,
                                     int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
-                                    cudaStream_t stream);
+                                    cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1);
 
 cudaError_t launch_flop_count(const uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
                               int64_t *counts, cudaStream_t stream);

@@ -67,22 +67,30 @@ __global__ void __launch_bounds__(kThreads)
 quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__restrict__ k,
                    int8_t *__restrict__ q_codes, float *__restrict__ q_scales,
                    int8_t *__restrict__ k_codes, float *__restrict__ k_scales, int64_t batch,
-                   int64_t tokens, int64_t hq, int64_t hkv, int64_t q_ctas) {
+                   int64_t tokens, int64_t hq, int64_t hkv, int64_t q_ctas, int64_t t_lo,
+                   int64_t t_hi) {
     const int tid = threadIdx.x;
     if (blockIdx.x < q_ctas) {
-        const int64_t q_rows = batch * tokens * hq;
+        // local Q rows (b, n in [t_lo, t_hi), h) -> global rows (b*N + n)*Hq + h
+        const int64_t span_rows = (t_hi - t_lo) * hq;
+        const int64_t q_rows = batch * span_rows;
         const int sub = tid % kLanesPerRow;
-        const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kQRowsPerCta + tid / kLanesPerRow;
+        const int64_t loc0 = static_cast<int64_t>(blockIdx.x) * kQRowsPerCta + tid / kLanesPerRow;
+        auto global_row = [&](int64_t loc) {
+            const int64_t b = loc / span_rows;
+            return (b * tokens + t_lo) * hq + (loc - b * span_rows);
+        };
         uint4 u[kQSlots];
 #pragma unroll
         for (int sl = 0; sl < kQSlots; ++sl) {
-            const int64_t row = row0 + sl * (kThreads / kLanesPerRow);
-            u[sl] = row < q_rows ? __ldcs(reinterpret_cast<const uint4 *>(q + row * kHeadDim) + sub)
+            const int64_t loc = loc0 + sl * (kThreads / kLanesPerRow);
+            u[sl] = loc < q_rows ? __ldcs(reinterpret_cast<const uint4 *>(q + global_row(loc) * kHeadDim) + sub)
                                  : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int sl = 0; sl < kQSlots; ++sl) {
-            const int64_t row = row0 + sl * (kThreads / kLanesPerRow);
+            const int64_t loc = loc0 + sl * (kThreads / kLanesPerRow);
+            const int64_t row = loc < q_rows ? global_row(loc) : 0;
             float f[8];
             unpack8(u[sl], f);
             float peak = 0.0f;
@@ -90,7 +98,7 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
             for (int i = 0; i < 8; ++i) peak = fmaxf(peak, fabsf(f[i]));
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
-            if (row >= q_rows) continue;
+            if (loc >= q_rows) continue;
             const float scale = scale_of(peak);
             const float inv = 1.0f / scale;
             uint32_t c[8];
@@ -110,11 +118,12 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
     }
     // ---- K group
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
+    const int64_t j_lo = t_lo / kBlockK, nj = (t_hi + kBlockK - 1) / kBlockK - j_lo;
     const uint32_t grp = static_cast<uint32_t>(static_cast<int64_t>(blockIdx.x) - q_ctas);
-    const uint32_t hkv32 = static_cast<uint32_t>(hkv), nk32 = static_cast<uint32_t>(nk);
+    const uint32_t hkv32 = static_cast<uint32_t>(hkv), nj32 = static_cast<uint32_t>(nj);
     const int64_t h = grp % hkv32;
-    const int64_t j = (grp / hkv32) % nk32;
-    const int64_t b = grp / (hkv32 * nk32);
+    const int64_t j = j_lo + (grp / hkv32) % nj32;
+    const int64_t b = grp / (hkv32 * nj32);
     const int r = tid >> 3;         // token within the block (0..31)
     const int sub = (tid & 7) * 2;  // two 8-element chunks: 16 elements
     const int64_t tok = j * kBlockK + r;
@@ -158,17 +167,20 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
 
 cudaError_t launch_quantize_qk(const void *q, const void *k, int8_t *q_codes, float *q_scales,
                                int8_t *k_codes, float *k_scales, int64_t batch, int64_t tokens,
-                               int64_t hq, int64_t hkv, cudaStream_t stream) {
-    const int64_t q_rows = q ? batch * tokens * hq : 0;
+                               int64_t hq, int64_t hkv, cudaStream_t stream, int64_t t_lo,
+                               int64_t t_hi) {
+    if (t_hi < 0) t_hi = tokens;
+    if (t_lo % kBlockK != 0 || t_lo < 0 || t_hi > tokens || t_lo >= t_hi) return cudaErrorInvalidValue;
+    const int64_t q_rows = q ? batch * (t_hi - t_lo) * hq : 0;
     const int64_t q_ctas = (q_rows + kQRowsPerCta - 1) / kQRowsPerCta;
-    if (q_rows > 0x7FFFFFFF) return cudaErrorInvalidValue; // 32-bit scale index math
-    const int64_t k_ctas = k ? batch * ((tokens + kBlockK - 1) / kBlockK) * hkv : 0;
+    if (batch * tokens * hq > 0x7FFFFFFF) return cudaErrorInvalidValue; // 32-bit scale index math
+    const int64_t k_ctas = k ? batch * ((t_hi + kBlockK - 1) / kBlockK - t_lo / kBlockK) * hkv : 0;
     const int64_t grid = q_ctas + k_ctas;
     if (grid == 0) return cudaSuccess;
     if (grid > 0x7FFFFFFF) return cudaErrorInvalidValue;
     quantize_qk_kernel<<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
         static_cast<const __nv_bfloat16 *>(q), static_cast<const __nv_bfloat16 *>(k), q_codes,
-        q_scales, k_codes, k_scales, batch, tokens, hq, hkv, q_ctas);
+        q_scales, k_codes, k_scales, batch, tokens, hq, hkv, q_ctas, t_lo, t_hi);
     return cudaGetLastError();
 }
 

@@ -94,7 +94,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
                         int64_t tokens, int64_t hq, int64_t hkv, float inv_sqrt_d,
                         const double *__restrict__ taus, float *__restrict__ thresh,
                         double *__restrict__ dbg_m, double *__restrict__ dbg_l,
-                        double *__restrict__ dbg_bound) {
+                        double *__restrict__ dbg_bound, int64_t i_first) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     StatsSmem &sm = *reinterpret_cast<StatsSmem *>(smem_raw);
     const int tid = threadIdx.x;
@@ -103,7 +103,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     tp[0] = prof ? clock64() : 0;
 #define SALE_PHASE(n) \
     if (prof) tp[n] = clock64();
-    const int64_t i = blockIdx.x + 3;
+    const int64_t i = blockIdx.x + i_first;
     const int64_t h = blockIdx.y;
     const int64_t b = blockIdx.z;
     const int64_t g = h / (hq / hkv);
@@ -311,11 +311,14 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
 // for i >= 3 and every causal block for i <= 2 (selection.hpp:228-245, :188).
 // One thread per 32-bit word. Middle segments are OR-ed in by K2b.
 __global__ void base_mask_kernel(uint32_t *__restrict__ mask, int64_t rows, int64_t nq,
-                                 int64_t nk, int64_t words, int64_t tokens) {
-    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= rows * words) return;
-    const int64_t w = idx % words;
-    const int64_t i = (idx / words) % nq;
+                                 int64_t nk, int64_t words, int64_t tokens, int64_t i_lo,
+                                 int64_t ni) {
+    const int64_t loc = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (loc >= rows * ni * words) return;
+    const int64_t w = loc % words;
+    const int64_t i = i_lo + (loc / words) % ni;
+    const int64_t bh = loc / (words * ni);
+    const int64_t idx = (bh * nq + i) * words + w;
     const int64_t fr = frontier_block(i, tokens, nk);
     const int64_t lo = i >= 3 ? 1 + kSegment * full_segments(i) : 0;
     uint32_t bits = 0;
@@ -331,9 +334,11 @@ __global__ void base_mask_kernel(uint32_t *__restrict__ mask, int64_t rows, int6
 cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch, int64_t tokens,
                                     int64_t hq, int64_t hkv, float inv_sqrt_d, const double *taus,
                                     float *thresh, double *dbg_m, double *dbg_l, double *dbg_bound,
-                                    cudaStream_t stream) {
+                                    cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
-    if (nq <= 3) return cudaSuccess;
+    if (i_hi < 0 || i_hi > nq) i_hi = nq;
+    const int64_t i_first = i_lo > 3 ? i_lo : 3; // blocks with a non-empty middle
+    if (i_hi <= i_first) return cudaSuccess;
     static bool configured = false;
     const size_t smem = sizeof(StatsSmem);
     if (!configured) {
@@ -343,24 +348,26 @@ cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch,
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid(static_cast<unsigned>(nq - 3), static_cast<unsigned>(hq),
+    dim3 grid(static_cast<unsigned>(i_hi - i_first), static_cast<unsigned>(hq),
               static_cast<unsigned>(batch));
     sink_local_stats_kernel<<<grid, kThreads, smem, stream>>>(
         static_cast<const __nv_bfloat16 *>(q), static_cast<const __nv_bfloat16 *>(k), tokens, hq,
-        hkv, inv_sqrt_d, taus, thresh, dbg_m, dbg_l, dbg_bound);
+        hkv, inv_sqrt_d, taus, thresh, dbg_m, dbg_l, dbg_bound, i_first);
     return cudaGetLastError();
 }
 
 cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t words = (nk + 31) / 32;
-    const int64_t total = batch * hq * nq * words;
+    if (i_hi < 0 || i_hi > nq) i_hi = nq;
+    if (i_hi <= i_lo) return cudaSuccess;
+    const int64_t total = batch * hq * (i_hi - i_lo) * words;
     const int threads = 256;
     const int64_t blocks = (total + threads - 1) / threads;
-    base_mask_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(mask, batch * hq * nq,
-                                                                           nq, nk, words, tokens);
+    base_mask_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
+        mask, batch * hq, nq, nk, words, tokens, i_lo, i_hi - i_lo);
     return cudaGetLastError();
 }
 

@@ -277,6 +277,22 @@ def test_prefill_matches_stages_and_host_path(torch):
     np.testing.assert_array_equal(host_out, _to_np(out.view(torch.int16)).view(np.uint16))
 
 
+@pytest.mark.parametrize("B,N,Hq,Hkv", [(1, 16384, 8, 2), (2, 20000, 4, 1), (3, 3000, 7, 1)])
+def test_chunked_host_pipeline_bit_identical(torch, B, N, Hq, Hkv):
+    """sale_b200_prefill_host streams token chunks through three streams (H2D /
+    kernels / D2H overlap, 8 chunks at >= 16K tokens, 4 at >= 2K); every stage
+    reads only its own and earlier chunks, so the output equals the one-shot
+    device prefill bit for bit (batch > 1 exercises the strided 2-D copies)."""
+    inp = Inputs("sink_local", 9, B, N, Hq, Hkv)
+    q, k, v = inp.torch()
+    taus = [0.004 * (1 + h % 3) for h in range(Hq)]
+    out = sale.prefill(q, k, v, taus)
+    host_out = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
+    pin = lambda a: torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).pin_memory()
+    sale.prefill_host(pin(inp.q16), pin(inp.k16), pin(inp.v16), taus, host_out)
+    assert torch.equal(host_out.view(torch.int16), out.cpu().view(torch.int16))
+
+
 def test_invalid_arguments(torch):
     inp = Inputs("gaussian", 1, 1, 256, 4, 2)
     q, k, v = inp.torch()
