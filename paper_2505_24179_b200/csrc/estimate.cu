@@ -58,10 +58,16 @@ struct EstSmem {
 // issuer spends blocked on K stages / accumulator buffers, and the epilogue on
 // accumulators. Off unless enabled; one global flag read per CTA.
 __device__ int g_est_prof_on = 0;
+static int g_est_mode_host = 0; // host copy: which kernel instance launches
 __device__ unsigned long long g_est_prof[8];
 
 namespace {
 
+// kMode: 0 production, 1 parity debug (block maxima out), 2 cycle profiling,
+// 3 profiling with the epilogue work skipped. The epilogue's per-head path is
+// latency-critical (every extra instruction there costs issue slack; see
+// profiles/README.md), so the diagnostics are separate instances.
+template <int kMode>
 __global__ void __launch_bounds__(kEstThreads, 1)
 estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_kc,
                 const EstUnit *__restrict__ units, const float *__restrict__ q_scales,
@@ -132,7 +138,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             uint64_t adesc[kEstHeads];
             for (int hh = 0; hh < kEstHeads; ++hh)
                 adesc[hh] = umma_desc_sw128(smem_u32(sm.a[hh]), 16, 1024);
-            const bool prof = g_est_prof_on != 0;
+            constexpr bool prof = kMode >= 2;
             long long t_start = clock64(), w_full = 0, w_empty = 0;
             mbar_wait(&sm.a_full, 0);
             const long long w_a = clock64() - t_start;
@@ -195,10 +201,10 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         for (int x = threadIdx.x - 128; x < kSegment * nstages; x += 32 * kEpiWarps)
             sm.ks[x] = ks_row[jb_base + x];
         named_bar_sync(1, 32 * kEpiWarps);
-        const bool dbg = dbg_max != nullptr && row_ok;
-        const bool epi_skip = g_est_prof_on == 2;
+        const bool dbg = kMode == 1 && row_ok;
+        constexpr bool epi_skip = kMode == 3;
         const uint32_t acc = tmem + (static_cast<uint32_t>(quad * 32) << 16) + 32 * chunk;
-        const bool prof = ew == 0 && g_est_prof_on != 0;
+        const bool prof = kMode >= 2 && ew == 0;
         long long w_epi = 0;
         const long long t_epi = clock64();
         // per-row selection flags: bit k of flags[hh][k >> 5] = some column of
@@ -219,11 +225,13 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
 #pragma unroll
             for (int hh = 0; hh < kEstHeads; ++hh) {
                 if (hh >= nh) break; // warp-uniform
-                const long long t0 = prof ? clock64() : 0;
+                long long t0 = 0;
+                if constexpr (kMode >= 2) t0 = prof ? clock64() : 0;
                 mbar_wait(&sm.tmem_full[hh], k & 1);
-                if (prof) w_epi += clock64() - t0;
+                if constexpr (kMode >= 2)
+                    if (prof) w_epi += clock64() - t0;
                 tc_fence_after();
-                if (epi_skip) { // diagnostic (profile mode 2): MMA side alone
+                if constexpr (epi_skip) { // diagnostic (profile mode 2): MMA side alone
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]);
@@ -247,8 +255,8 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 const bool pass = est >= fb[hh];
                 flags[hh][0] |= pass ? kb0 : 0u;
                 flags[hh][1] |= pass ? kb1 : 0u;
-                if (dbg)
-                    dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                if constexpr (kMode == 1)
+                    if (dbg) dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
                             jb_base + 4 * k + chunk] = mx;
             }
         }
@@ -306,6 +314,7 @@ cudaError_t estimate_profile(int enable, unsigned long long *out8) {
     unsigned long long zero[8] = {};
     cudaError_t e = cudaMemcpyToSymbol(g_est_prof, zero, sizeof(zero));
     if (e != cudaSuccess) return e;
+    g_est_mode_host = enable;
     return cudaMemcpyToSymbol(g_est_prof_on, &enable, sizeof(int));
 }
 
@@ -315,21 +324,22 @@ cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, 
                             int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
                             cudaStream_t stream) {
     if (n_units == 0) return cudaSuccess;
-    static bool configured = false;
     const size_t smem = estimate_smem_bytes();
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(estimate_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const int mode = dbg_max ? 1 : (g_est_mode_host == 0 ? 0 : (g_est_mode_host == 2 ? 3 : 2));
+    auto kern = mode == 0 ? estimate_kernel<0> : mode == 1 ? estimate_kernel<1>
+                                            : mode == 2 ? estimate_kernel<2> : estimate_kernel<3>;
+    static bool configured[4] = {false, false, false, false};
+    if (!configured[mode]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured[mode] = true;
     }
     const int group = hq / hkv;
     const int nsub = (group + kEstHeads - 1) / kEstHeads;
     dim3 grid(static_cast<unsigned>(n_units), static_cast<unsigned>(batch * hkv * nsub));
-    estimate_kernel<<<grid, kEstThreads, smem, stream>>>(tm_qc, tm_kc, units, q_scales, k_scales,
-                                                         thresh, mask, tokens, hq, hkv, nsub,
-                                                         inv_sqrt_d, dbg_max);
+    kern<<<grid, kEstThreads, smem, stream>>>(tm_qc, tm_kc, units, q_scales, k_scales, thresh, mask,
+                                              tokens, hq, hkv, nsub, inv_sqrt_d, dbg_max);
     return cudaGetLastError();
 }
 
