@@ -239,10 +239,9 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 }
                 uint32_t v[16];
                 tmem_ld32_pack16(acc + 128 * hh, v);
-                tmem_ld_wait();
+                tmem_ld_wait(); // warp-collective: every lane's values are in registers
                 tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]); // registers hold the data now
+                if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]);
 #pragma unroll
                 for (int s = 8; s > 0; s >>= 1)
 #pragma unroll
