@@ -31,12 +31,12 @@ namespace sale_b200 {
 
 constexpr int kSegPerUnit = 64;            // segments per work unit (8192 keys)
 constexpr int kSegWords = kSegPerUnit / 32;
-constexpr int kEstHeads = 4;               // query heads per CTA
-constexpr int kEstStages = 6;              // TMA ring depth
+constexpr int kEstHeads = 2;               // query heads per CTA (two CTAs per SM)
+constexpr int kEstStages = 4;              // TMA ring depth
 constexpr int kStageKeys = kSegment * kBlockK;       // 128 keys = one segment
 constexpr int kATileBytes = 128 * kHeadDim;          // 16 KB per head
 constexpr int kBStageBytes = kStageKeys * kHeadDim;  // 16 KB
-constexpr int kEpiWarps = 16;              // one (lane quadrant, query head) per warp
+constexpr int kEpiWarps = 8;               // (lane quadrant, pair of key blocks) per warp
 constexpr int kEstThreads = 128 + 32 * kEpiWarps; // warps 0-3 control, 4-19 epilogue
 
 static_assert(kSegPerUnit == kSegPerUnitHost, "unit size mismatch");
@@ -68,7 +68,7 @@ namespace {
 // latency-critical (every extra instruction there costs issue slack; see
 // profiles/README.md), so the diagnostics are separate instances.
 template <int kMode>
-__global__ void __launch_bounds__(kEstThreads, 1)
+__global__ void __launch_bounds__(kEstThreads, 2)
 estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_kc,
                 const EstUnit *__restrict__ units, const float *__restrict__ q_scales,
                 const float *__restrict__ k_scales, const float *__restrict__ thresh,
@@ -110,7 +110,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                 for (int w = 0; w < kSegWords; ++w) sm.seg_bits[hh][x][w] = 0;
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+    if (warp == 2) tmem_alloc<kEstHeads * 128>(&sm.tmem_base);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -181,9 +181,9 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const int r = quad * 32 + lane;       // row within the 128-row tile
         const int64_t tok = row0 + r;
         const bool row_ok = tok < tokens;
-        // Every head's buffer is drained by all 16 warps: warp = (quadrant,
-        // key block `chunk` of the segment = 32 accumulator columns).
-        const int chunk = ew >> 2;
+        // Every head's buffer is drained by all 8 warps: warp = (quadrant, key
+        // blocks chunk, chunk + 1 of the segment = 64 accumulator columns).
+        const int chunk = 2 * (ew >> 2);
         float qs[kEstHeads], fb[kEstHeads];
 #pragma unroll
         for (int hh = 0; hh < kEstHeads; ++hh) {
@@ -215,7 +215,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
 #pragma unroll
             for (int w = 0; w < kSegWords; ++w) flags[hh][w] = 0u;
         for (int k = 0; k < nstages; ++k) {
-            const float ks = sm.ks[4 * k + chunk];
+            const float ks = sm.ks[4 * k + chunk], ks1 = sm.ks[4 * k + chunk + 1];
             const uint32_t kbit = 1u << (k & 31);
             const uint32_t kb0 = (k >> 5) == 0 ? kbit : 0u, kb1 = kbit ^ kb0;
             static_assert(kSegWords == 2, "flag words");
@@ -237,26 +237,35 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                     if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]);
                     continue;
                 }
-                uint32_t v[16];
-                tmem_ld32_pack16(acc + 128 * hh, v);
+                uint32_t v[32];
+                tmem_ld64_pack16(acc + 128 * hh, v);
                 tmem_ld_wait(); // warp-collective: every lane's values are in registers
                 tc_fence_before();
                 if (lane == 0) mbar_arrive(&sm.tmem_empty[hh]);
+                // int16 pairs: v[0..15] key block chunk, v[16..31] chunk + 1
 #pragma unroll
                 for (int s = 8; s > 0; s >>= 1)
 #pragma unroll
-                    for (int e = 0; e < s; ++e) v[e] = __vmaxs2(v[e], v[e + s]);
-                const int lo = static_cast<int16_t>(v[0] & 0xFFFFu);
-                const int hi = static_cast<int16_t>(v[0] >> 16);
-                const int mx = lo > hi ? lo : hi;
-                const float rs = __fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d);
-                const float est = __fmul_rn(rs, static_cast<float>(mx));
-                const bool pass = est >= fb[hh];
+                    for (int e = 0; e < s; ++e) {
+                        v[e] = __vmaxs2(v[e], v[e + s]);
+                        v[16 + e] = __vmaxs2(v[16 + e], v[16 + e + s]);
+                    }
+                const int mx0 = max(static_cast<int>(static_cast<int16_t>(v[0] & 0xFFFFu)),
+                                    static_cast<int>(static_cast<int16_t>(v[0] >> 16)));
+                const int mx1 = max(static_cast<int>(static_cast<int16_t>(v[16] & 0xFFFFu)),
+                                    static_cast<int>(static_cast<int16_t>(v[16] >> 16)));
+                const float est0 = __fmul_rn(__fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d), static_cast<float>(mx0));
+                const float est1 = __fmul_rn(__fmul_rn(__fmul_rn(qs[hh], ks1), inv_sqrt_d), static_cast<float>(mx1));
+                const bool pass = est0 >= fb[hh] || est1 >= fb[hh];
                 flags[hh][0] |= pass ? kb0 : 0u;
                 flags[hh][1] |= pass ? kb1 : 0u;
                 if constexpr (kMode == 1)
-                    if (dbg) dbg_max[((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                            jb_base + 4 * k + chunk] = mx;
+                    if (dbg) {
+                        int32_t *dm = dbg_max + ((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
+                                      jb_base + 4 * k + chunk;
+                        dm[0] = mx0;
+                        dm[1] = mx1;
+                    }
             }
         }
         // OR over the warp's 32 rows; the two query blocks of the tile are the
@@ -297,7 +306,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem);
+        tmem_dealloc<kEstHeads * 128>(tmem);
     }
 }
 
