@@ -23,7 +23,7 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", "
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 ix = {h: i for i, h in enumerate(hdr)}
-name = lambda r: r[ix["Kernel Name"]].split("(")[0].split("::")[-1]
+name = lambda r: r[ix["Kernel Name"]].split("(")[0].split("::")[-1].split("<")[0]
 lines = ["| kernel | " + " | ".join(f"{m} ({units[ix[m]]})" for m in METRICS) + " |",
          "|---|" + "---|" * len(METRICS)]
 traffic = {}
