@@ -44,14 +44,12 @@ constexpr uint32_t kColO = 0, kColS0 = 128, kColQ = 384;
 struct AttnSmem {
     alignas(1024) uint8_t k[kKvStages][2][kTileBytesHalf];
     alignas(1024) uint8_t v[kKvStages][2][kTileBytesHalf];
-    uint64_t q_ready, k_full[kKvStages], v_full[kKvStages], kv_empty[kKvStages];
+    uint64_t q_ready, k_full[kKvStages], v_full[kKvStages], k_empty[kKvStages], v_empty[kKvStages];
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
     int ntiles;
     int warp_cnt[kAttnThreads / 32];
-    float xch[2][2][128];   // [tile parity][column half][row]: partial row max
-    float fin_l[128];       // end: column-half-1 partial l and coverage
-    int fin_cov[128];
+    long long prof_tp[4];      // profiling: MMA-side time P_j was observed (ring)
     uint32_t tiles[kMaxTiles]; // j | bits8 << 16
 };
 
@@ -107,123 +105,125 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&p);
 }
 
-// O (this thread's 64-column half) *= alpha, once PV of every earlier tile has
-// landed in O.
-__device__ __forceinline__ void rescale_o(uint32_t oAddr, float alpha, uint64_t *pv_prev,
-                                          uint32_t pv_parity) {
+// O rows of this warp (16 TMEM lanes: thread rows T/4, T/4+8) *= alpha per
+// row, once PV of every earlier tile has landed in O.
+__device__ __forceinline__ void rescale_o16(uint32_t oAddr, float a0, float a1, uint64_t *pv_prev,
+                                            uint32_t pv_parity) {
     mbar_wait(pv_prev, pv_parity);
     tc_fence_after();
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
         uint32_t o[32];
-        tmem_ld32(oAddr + 32 * cc, o);
+        tmem_ld16x256_x8(oAddr + 64 * cc, o);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-        tmem_st32(oAddr + 32 * cc, o);
+        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * ((e & 2) ? a1 : a0));
+        tmem_st16x256_x8(oAddr + 64 * cc, o);
     }
     tmem_st_wait();
 }
 
 struct SoftmaxState {
-    float m_run = -INFINITY; // running max, exp2 domain (logit * scale_log2)
-    float l_run = 0.0f;      // running sum of p over this thread's column half
-    int cov = 0;             // attended tokens in this thread's column half
+    float m[2] = {-INFINITY, -INFINITY}; // running max per row, exp2 domain (logit * scale_log2)
+    float l[2] = {0.0f, 0.0f};           // running sum of p over this thread's columns
+    int cov[2] = {0, 0};                 // attended tokens in this thread's columns
 };
 
-// One S tile, one row, one column half (thread). The two softmax warpgroups
-// split every tile's columns: warpgroup w owns tile columns [NC*w, NC*w + NC)
-// (NC = 64 for segment tiles; the 32-key sink tile is all warpgroup 0's, NC = 32,
-// and warpgroup 1 takes NC = 0). The row max is combined through shared memory
-// (xch, one named barrier per lane quadrant = the two warps that own the same
-// TMEM lanes); each half keeps its own partial l and coverage, summed at the
-// end. Both halves therefore see the same running max and take the same lazy
-// rescale decisions. S holds raw fp32 logits*sqrt(d); the bf16 P pairs of
-// columns [c0, c0+NC) are written to TMEM columns [c0/2, c0/2 + NC/2) of the
-// same buffer (written only after the barrier, i.e. after both halves have
-// read their S columns).
-template <int NC>
-__device__ __forceinline__ void softmax_part(uint32_t sAddr, uint32_t pAddr, uint32_t oAddr,
-                                             uint32_t nib, int64_t lim, float scale_log2,
-                                             SoftmaxState &st, float *xch_mine,
-                                             const float *xch_other, uint32_t bar_id,
-                                             uint64_t *pv_prev, uint32_t pv_parity) {
-    constexpr int NS = NC / 32 > 0 ? NC / 32 : 1; // 32-key sub-blocks in this half
-    // nib: this half's sub-block bits; lim: valid columns c <= lim (half-relative)
-    const bool any_valid = NC > 0 && nib != 0u && lim >= 0;
-    const bool zero = __all_sync(0xffffffffu, !any_valid);
-    uint32_t s[NC > 0 ? NC : 1];
-    float mt = -INFINITY;
-    int nvalid = 0;
-    bool full = false;
-    if constexpr (NC > 0) {
-        if (!zero) {
+// One S tile for the 16 rows of this warp. Thread T owns rows T/4 and T/4+8
+// of the warp's TMEM lanes and columns 8R + 2(T%4) + {0,1} (R < 16) of each:
+// the row max is combined over the four threads of a row by two shuffles, so
+// the two warps sharing a TMEM lane quadrant never synchronise with each other.
+// nib: the row head's four 32-key sub-block bits of this tile; lim0/lim1:
+// valid columns c <= lim per row (-1: none). S holds raw fp32 logits*sqrt(d);
+// the bf16 P pairs go to columns [0, 64) of the same buffer (only this warp's
+// lanes, whose S values are already in registers).
+__device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uint32_t nib,
+                                             int64_t lim0, int64_t lim1, int q4, float scale_log2,
+                                             SoftmaxState &st, uint64_t *pv_prev, uint32_t pv_parity) {
+    const bool any_valid = nib != 0u && (lim0 >= 0 || lim1 >= 0);
+    uint32_t s[64];
+    if (__all_sync(0xffffffffu, !any_valid)) {
+        // nothing of this tile is attended by the warp's rows: P = 0, no exp work
 #pragma unroll
-            for (int c4 = 0; c4 < NC / 32; ++c4)
-                tmem_ld32(sAddr + 32 * c4, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c4]));
-            tmem_ld_wait();
-            full = nib == ((1u << NS) - 1u) && lim >= NC - 1;
-            nvalid = NC;
-            if (!full) {
-                nvalid = 0;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const bool ok = ((nib >> (c >> 5)) & 1u) && c <= lim;
-                    s[c] = ok ? s[c] : __float_as_uint(-INFINITY);
-                    nvalid += ok ? 1 : 0;
-                }
-            }
-            // four independent max chains (latency), then combined
-            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-            for (int c = 0; c < NC; c += 8)
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    mx[u] = fmax3(mx[u], __uint_as_float(s[c + 2 * u]), __uint_as_float(s[c + 2 * u + 1]));
-            mt = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
-        }
+        for (int e = 0; e < 32; ++e) s[e] = 0u;
+        tmem_st16x128_x16(sAddr, s);
+        tmem_st_wait();
+        return;
     }
-    // combine the row max with the other column half
-    *xch_mine = mt;
-    named_bar_sync(bar_id, 64);
-    mt = fmaxf(mt, *xch_other);
-    const float m_new = fmaxf(st.m_run, mt * scale_log2);
+    tmem_ld16x256_x8(sAddr, s);
+    tmem_ld16x256_x8(sAddr + 64, s + 32);
+    tmem_ld_wait();
+    const bool full = nib == 0xFu && lim0 >= 127 && lim1 >= 127;
+    int nv0 = 64, nv1 = 64;
+    if (!full) {
+        nv0 = nv1 = 0;
+#pragma unroll
+        for (int R = 0; R < 16; ++R)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t c = 8 * R + 2 * q4 + e;
+                const bool sub = (nib >> (R >> 2)) & 1u;
+                const bool ok0 = sub && c <= lim0, ok1 = sub && c <= lim1;
+                s[4 * R + e] = ok0 ? s[4 * R + e] : __float_as_uint(-INFINITY);
+                s[4 * R + 2 + e] = ok1 ? s[4 * R + 2 + e] : __float_as_uint(-INFINITY);
+                nv0 += ok0 ? 1 : 0;
+                nv1 += ok1 ? 1 : 0;
+            }
+    } else {
+        nv0 = nv1 = 32;
+    }
+    // row max: two chains per row, then the four threads of the row
+    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int R = 0; R < 16; R += 2) {
+        mx[0] = fmax3(mx[0], __uint_as_float(s[4 * R]), __uint_as_float(s[4 * R + 1]));
+        mx[1] = fmax3(mx[1], __uint_as_float(s[4 * R + 4]), __uint_as_float(s[4 * R + 5]));
+        mx[2] = fmax3(mx[2], __uint_as_float(s[4 * R + 2]), __uint_as_float(s[4 * R + 3]));
+        mx[3] = fmax3(mx[3], __uint_as_float(s[4 * R + 6]), __uint_as_float(s[4 * R + 7]));
+    }
+    float t0 = fmaxf(mx[0], mx[1]), t1 = fmaxf(mx[2], mx[3]);
+    t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, 1));
+    t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, 1));
+    t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, 2));
+    t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, 2));
     // lazy rescale: only when the running max grows by > 8 (exp2 domain); P is
-    // computed against the new max, O and l are rescaled after P is stored
-    // (fewer live registers), before p_full releases PV of this tile.
-    const bool need = st.m_run != -INFINITY && m_new > st.m_run + 8.0f;
-    const float alpha = need ? ex2_approx(st.m_run - m_new) : 1.0f;
-    if (st.m_run == -INFINITY || need) st.m_run = m_new;
-    if (need) st.l_run *= alpha;
-    const bool any_need = __any_sync(0xffffffffu, need);
-    if constexpr (NC > 0) {
-        if (zero) {
-            // nothing of this half is attended by the warp's rows: P = 0, no exp work
-            uint32_t z[32];
+    // computed against the new max, O is rescaled after P is stored (fewer
+    // live registers), before p_full releases PV of this tile.
+    float alpha[2];
+    bool need_any = false;
+    const float tm[2] = {t0, t1};
 #pragma unroll
-            for (int e = 0; e < 32; ++e) z[e] = 0u;
-            if constexpr (NC == 64) tmem_st32(pAddr, z);
-            else tmem_st16(pAddr, *reinterpret_cast<uint32_t(*)[16]>(&z[0]));
-            tmem_st_wait();
-            if (any_need) rescale_o(oAddr, alpha, pv_prev, pv_parity);
-            return;
-        }
-        // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
-        // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
-        const float neg_m = st.m_run == -INFINITY ? 0.0f : -st.m_run;
-        const unsigned long long sc2 = pack_f2(scale_log2, scale_log2), nm2 = pack_f2(neg_m, neg_m);
-        unsigned long long psum2 = 0ull;
-        if (NC == 64 && __all_sync(0xffffffffu, full)) {
-            // Full halves: every second pair takes exp2 on the FMA/ALU pipes
-            // (Cody-Waite split + degree-3 polynomial, rel. err 1e-4 < bf16's
-            // 2^-8), the rest on MUFU (16 ex2/clk/SM): per SMSP and tile the XU,
-            // FMA and ALU pipes then carry about equal work.
+    for (int k = 0; k < 2; ++k) {
+        const float m_new = fmaxf(st.m[k], tm[k] * scale_log2);
+        const bool need = st.m[k] != -INFINITY && m_new > st.m[k] + 8.0f;
+        alpha[k] = need ? ex2_approx(st.m[k] - m_new) : 1.0f;
+        if (st.m[k] == -INFINITY || need) st.m[k] = m_new;
+        if (need) st.l[k] *= alpha[k];
+        need_any |= need;
+    }
+    const bool any_need = __any_sync(0xffffffffu, need_any);
+    // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
+    // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
+    const unsigned long long sc2 = pack_f2(scale_log2, scale_log2);
+    unsigned long long nm2[2], psum2[2] = {0ull, 0ull};
 #pragma unroll
-            for (int c2 = 0; c2 < NC / 2; ++c2) {
-                unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
-                ffma2_f32(x, sc2, nm2);
+    for (int k = 0; k < 2; ++k) {
+        const float neg_m = st.m[k] == -INFINITY ? 0.0f : -st.m[k];
+        nm2[k] = pack_f2(neg_m, neg_m);
+    }
+    if (__all_sync(0xffffffffu, full)) {
+        // Full tiles: the pairs of odd R take exp2 on the FMA/ALU pipes
+        // (Cody-Waite split + degree-3 polynomial, rel. err 1e-4 < bf16's
+        // 2^-8), the rest on MUFU (16 ex2/clk/SM).
+#pragma unroll
+        for (int R = 0; R < 16; ++R)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                unsigned long long x =
+                    (static_cast<unsigned long long>(s[4 * R + 2 * k + 1]) << 32) | s[4 * R + 2 * k];
+                ffma2_f32(x, sc2, nm2[k]);
                 float p0, p1;
-                if (c2 & 1) {
+                if (R & 1) {
                     const unsigned long long xc =
                         pack_f2(fmaxf(__uint_as_float(static_cast<uint32_t>(x)), -125.0f),
                                 fmaxf(__uint_as_float(static_cast<uint32_t>(x >> 32)), -125.0f));
@@ -245,28 +245,32 @@ __device__ __forceinline__ void softmax_part(uint32_t sAddr, uint32_t pAddr, uin
                     p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
                     p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
                 }
-                fadd2_f32(psum2, pack_f2(p0, p1));
-                s[c2] = pack_bf16x2(p0, p1);
+                fadd2_f32(psum2[k], pack_f2(p0, p1));
+                s[2 * R + k] = pack_bf16x2(p0, p1); // in place: index 2R+k was already consumed
             }
-        } else {
+    } else {
 #pragma unroll
-            for (int c2 = 0; c2 < NC / 2; ++c2) {
-                unsigned long long x = (static_cast<unsigned long long>(s[2 * c2 + 1]) << 32) | s[2 * c2];
-                ffma2_f32(x, sc2, nm2); // x = x * scale + (-m), two lanes
+        for (int R = 0; R < 16; ++R)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                unsigned long long x =
+                    (static_cast<unsigned long long>(s[4 * R + 2 * k + 1]) << 32) | s[4 * R + 2 * k];
+                ffma2_f32(x, sc2, nm2[k]); // x = x * scale + (-m), two lanes
                 const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
                 const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
-                fadd2_f32(psum2, pack_f2(p0, p1));
-                s[c2] = pack_bf16x2(p0, p1); // in place: s[c2] was consumed at step c2/2
+                fadd2_f32(psum2[k], pack_f2(p0, p1));
+                s[2 * R + k] = pack_bf16x2(p0, p1);
             }
-        }
-        st.l_run += __uint_as_float(static_cast<uint32_t>(psum2)) +
-                    __uint_as_float(static_cast<uint32_t>(psum2 >> 32));
-        st.cov += nvalid;
-        if constexpr (NC == 64) tmem_st32(pAddr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        else tmem_st16(pAddr, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
-        tmem_st_wait();
     }
-    if (any_need) rescale_o(oAddr, alpha, pv_prev, pv_parity);
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+        st.l[k] += __uint_as_float(static_cast<uint32_t>(psum2[k])) +
+                   __uint_as_float(static_cast<uint32_t>(psum2[k] >> 32));
+    st.cov[0] += nv0;
+    st.cov[1] += nv1;
+    tmem_st16x128_x16(sAddr, s);
+    tmem_st_wait();
+    if (any_need) rescale_o16(oAddr, alpha[0], alpha[1], pv_prev, pv_parity);
 }
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -306,7 +310,8 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         for (int s = 0; s < kKvStages; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.v_full[s], 1);
-            mbar_init(&sm.kv_empty[s], 1);
+            mbar_init(&sm.k_empty[s], 1);
+            mbar_init(&sm.v_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.s_full[s], 1);
@@ -366,17 +371,30 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         if (elect_one() && ntiles > 0) {
             tma_prefetch(&tm_k);
             tma_prefetch(&tm_v);
-            for (int jj = 0; jj < ntiles; ++jj) {
-                const int st = jj % kKvStages;
+            // K_jj is released by S_jj, V_jj by PV_jj (one tile later): K runs
+            // one tile ahead of V so a late PV never holds back the next K.
+            auto key0_of = [&](int jj) {
                 const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
-                const int key0 = j == 0 ? 0 : kBlockK + 128 * (j - 1);
-                mbar_wait(&sm.kv_empty[st], ((jj / kKvStages) & 1) ^ 1);
-                mbar_expect_tx(&sm.k_full[st], 2 * kTileBytesHalf);
-                tma_load_4d(sm.k[st][0], &tm_k, &sm.k_full[st], 0, g, key0, b);
-                tma_load_4d(sm.k[st][1], &tm_k, &sm.k_full[st], 64, g, key0, b);
-                mbar_expect_tx(&sm.v_full[st], 2 * kTileBytesHalf);
-                tma_load_4d(sm.v[st][0], &tm_v, &sm.v_full[st], 0, g, key0, b);
-                tma_load_4d(sm.v[st][1], &tm_v, &sm.v_full[st], 64, g, key0, b);
+                return j == 0 ? 0 : kBlockK + 128 * (j - 1);
+            };
+            for (int jj = 0; jj <= ntiles; ++jj) {
+                if (jj < ntiles) {
+                    const int st = jj % kKvStages;
+                    const int key0 = key0_of(jj);
+                    mbar_wait(&sm.k_empty[st], ((jj / kKvStages) & 1) ^ 1);
+                    mbar_expect_tx(&sm.k_full[st], 2 * kTileBytesHalf);
+                    tma_load_4d(sm.k[st][0], &tm_k, &sm.k_full[st], 0, g, key0, b);
+                    tma_load_4d(sm.k[st][1], &tm_k, &sm.k_full[st], 64, g, key0, b);
+                }
+                if (jj > 0) {
+                    const int vj = jj - 1;
+                    const int st = vj % kKvStages;
+                    const int key0 = key0_of(vj);
+                    mbar_wait(&sm.v_empty[st], ((vj / kKvStages) & 1) ^ 1);
+                    mbar_expect_tx(&sm.v_full[st], 2 * kTileBytesHalf);
+                    tma_load_4d(sm.v[st][0], &tm_v, &sm.v_full[st], 0, g, key0, b);
+                    tma_load_4d(sm.v[st][1], &tm_v, &sm.v_full[st], 64, g, key0, b);
+                }
             }
         }
     } else if (warp == 1) {
@@ -388,46 +406,64 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             long long w_k = 0, w_p = 0, w_v = 0, t0 = 0;
             mbar_wait(&sm.q_ready, 0);
             tc_fence_after();
-            for (int jj = 0; jj <= ntiles; ++jj) {
-                if (jj < ntiles) {
-                    const int st = jj % kKvStages;
-                    const int sb = jj & 1;
-                    const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
-                    const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
-                    if (prof) t0 = clock64();
-                    mbar_wait(&sm.k_full[st], (jj / kKvStages) & 1);
-                    if (prof) w_k += clock64() - t0;
-                    tc_fence_after();
-                    const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
-                    const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
-                    const uint32_t dS = tmem + kColS0 + 128u * static_cast<uint32_t>(sb);
+            // Order on the tensor pipe: S_0, S_1, PV_0, S_2, PV_1, S_3, ...
+            // S_{j+2} reuses S_j's buffer right behind PV_j (in-order pipe). The
+            // K / V readiness checks come before the P wait, so once P_j is seen
+            // PV_j and S_{j+2} issue with no further barrier latency.
+            auto issue_s = [&](int jj) {
+                const int st = jj % kKvStages;
+                const int sb = jj & 1;
+                const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
+                const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
+                const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
+                const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
+                const uint32_t dS = tmem + kColS0 + 128u * static_cast<uint32_t>(sb);
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) { // K = 16 bf16 = 8 TMEM columns of Q
-                        const uint64_t bd = (kk < 4 ? kd0 : kd1) + 2 * (kk & 3);
-                        mma_bf16_ts(dS, tmem + kColQ + 8 * kk, bd, idesc_s, kk > 0);
-                    }
-                    tc_commit(&sm.s_full[sb]);
+                for (int kk = 0; kk < 8; ++kk) { // K = 16 bf16 = 8 TMEM columns of Q
+                    const uint64_t bd = (kk < 4 ? kd0 : kd1) + 2 * (kk & 3);
+                    mma_bf16_ts(dS, tmem + kColQ + 8 * kk, bd, idesc_s, kk > 0);
                 }
-                if (jj > 0) {
-                    const int pj = jj - 1;
-                    const int pst = pj % kKvStages;
-                    const int psb = pj & 1;
-                    const int jp = static_cast<int>(sm.tiles[pj] & 0xFFFFu);
-                    const int steps = jp == 0 ? 2 : 8;
-                    if (prof) t0 = clock64();
-                    mbar_wait(&sm.p_full[psb], (pj >> 1) & 1);
-                    if (prof) { w_p += clock64() - t0; t0 = clock64(); }
-                    mbar_wait(&sm.v_full[pst], (pj / kKvStages) & 1);
-                    if (prof) w_v += clock64() - t0;
-                    tc_fence_after();
-                    const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
-                    const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(psb);
-                    for (int kk = 0; kk < steps; ++kk)
-                        mma_bf16_ts(tmem + kColO, aP + 8 * kk, vd + 128 * kk, // +16 keys = 2 KB
-                                    idesc_pv, (pj > 0 || kk > 0) ? 1u : 0u);
-                    tc_commit(&sm.kv_empty[pst]);
-                    tc_commit(&sm.pv_done[psb]);
+                tc_commit(&sm.s_full[sb]);
+                tc_commit(&sm.k_empty[st]);
+            };
+            auto wait_k = [&](int jj) {
+                if (prof) t0 = clock64();
+                mbar_wait(&sm.k_full[jj % kKvStages], (jj / kKvStages) & 1);
+                if (prof) w_k += clock64() - t0;
+            };
+            wait_k(0);
+            tc_fence_after();
+            issue_s(0);
+            if (ntiles > 1) {
+                wait_k(1);
+                tc_fence_after();
+                issue_s(1);
+            }
+            for (int pj = 0; pj < ntiles; ++pj) {
+                const int nx = pj + 2;
+                const int pst = pj % kKvStages;
+                const int psb = pj & 1;
+                const int jp = static_cast<int>(sm.tiles[pj] & 0xFFFFu);
+                const int steps = jp == 0 ? 2 : 8;
+                if (nx < ntiles) wait_k(nx);
+                if (prof) t0 = clock64();
+                mbar_wait(&sm.v_full[pst], (pj / kKvStages) & 1);
+                if (prof) { w_v += clock64() - t0; t0 = clock64(); }
+                mbar_wait(&sm.p_full[psb], (pj >> 1) & 1);
+                if (prof) {
+                    const long long tn = clock64();
+                    w_p += tn - t0;
+                    *reinterpret_cast<volatile long long *>(&sm.prof_tp[pj & 3]) = tn;
                 }
+                tc_fence_after();
+                const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
+                const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(psb);
+                for (int kk = 0; kk < steps; ++kk)
+                    mma_bf16_ts(tmem + kColO, aP + 8 * kk, vd + 128 * kk, // +16 keys = 2 KB
+                                idesc_pv, (pj > 0 || kk > 0) ? 1u : 0u);
+                tc_commit(&sm.v_empty[pst]);
+                tc_commit(&sm.pv_done[psb]);
+                if (nx < ntiles) issue_s(nx);
             }
             if (prof) {
                 atomicAdd(&g_attn_prof[4], static_cast<unsigned long long>(clock64() - t_start));
@@ -447,7 +483,6 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         const int64_t grow = q0 + (r & 63);
         const bool row_ok = grow < tokens && (half == 0 || hasB);
         const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        const uint32_t bar_id = 1 + quad;
         // Q row half -> TMEM columns [kColQ + 32 wg, +32): the A operand of S = Q K^T
         {
             uint32_t a[32];
@@ -464,32 +499,43 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.q_ready);
         }
+        // softmax rows: warp (quad, wg) owns TMEM lanes quad*32 + 16 wg + [0, 16);
+        // thread rows rr0 = that + lane/4 and rr1 = rr0 + 8 (same head)
+        const int q4 = lane & 3;
+        const int rr0 = quad * 32 + 16 * wg + (lane >> 2);
+        const int64_t grow0 = q0 + (rr0 & 63), grow1 = grow0 + 8;
+        const bool ok0 = grow0 < tokens && (half == 0 || hasB);
+        const bool ok1 = grow1 < tokens && (half == 0 || hasB);
+        const uint32_t lane16 = tmem + (static_cast<uint32_t>(quad * 32 + 16 * wg) << 16);
         SoftmaxState st;
-        const uint32_t oAddr = lane_addr + kColO + 64u * wg;
+        const uint32_t oAddr = lane16 + kColO;
         const bool prof = warp == 3 && lane == 0 && g_attn_prof_on != 0;
         const long long t_loop = clock64();
-        long long w_s = 0, t_part = 0, t1 = 0;
+        long long w_s = 0, t_part = 0, t1 = 0, w_chain = 0, n_chain = 0;
         for (int jj = 0; jj < ntiles; ++jj) {
             const int sb = jj & 1;
             const uint32_t info = sm.tiles[jj];
             const int j = static_cast<int>(info & 0xFFFFu);
             const uint32_t nib = (info >> (16 + 4 * half)) & 0xFu;
             const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
-            const uint32_t sBase = lane_addr + kColS0 + 128u * sb;
-            float *xm = &sm.xch[sb][wg][r];
-            const float *xo = &sm.xch[sb][wg ^ 1][r];
             if (prof) t1 = clock64();
             mbar_wait(&sm.s_full[sb], (jj >> 1) & 1);
-            if (prof) { const long long t2 = clock64(); w_s += t2 - t1; t1 = t2; }
+            if (prof) {
+                const long long t2 = clock64();
+                w_s += t2 - t1;
+                t1 = t2;
+                if (jj >= 2) {
+                    w_chain += t2 - *reinterpret_cast<volatile long long *>(&sm.prof_tp[(jj - 2) & 3]);
+                    ++n_chain;
+                }
+            }
             tc_fence_after();
             const int pj = jj - 1;
-            // The 32-key sink tile runs through the same 64-column code: its
-            // columns >= 32 (stale S data) are masked like unselected sub-blocks,
-            // so warpgroup 1 always takes the zero path there.
-            const uint32_t nib_half = j == 0 ? (wg == 0 ? (nib & 1u) : 0u) : (nib >> (2 * wg)) & 3u;
-            const int64_t lim = row_ok ? grow - key0 - 64 * wg : -1;
-            softmax_part<64>(sBase + 64u * wg, sBase + 32u * wg, oAddr, nib_half, lim, scale_log2, st,
-                             xm, xo, bar_id, &sm.pv_done[pj & 1], (pj >> 1) & 1);
+            // The 32-key sink tile: columns >= 32 hold stale S data and are
+            // masked like unselected sub-blocks.
+            softmax_tile(lane16 + kColS0 + 128u * sb, oAddr, j == 0 ? (nib & 1u) : nib,
+                         ok0 ? grow0 - key0 : -1, ok1 ? grow1 - key0 : -1, q4, scale_log2, st,
+                         &sm.pv_done[pj & 1], (pj >> 1) & 1);
             if (prof) t_part += clock64() - t1;
             tc_fence_before();
             __syncwarp();
@@ -501,54 +547,54 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             atomicAdd(&g_attn_prof[1], static_cast<unsigned long long>(w_s));
             atomicAdd(&g_attn_prof[2], static_cast<unsigned long long>(t_part));
             atomicAdd(&g_attn_prof[3], static_cast<unsigned long long>(ntiles));
+            atomicAdd(&g_attn_prof[11], static_cast<unsigned long long>(w_chain));
+            atomicAdd(&g_attn_prof[12], static_cast<unsigned long long>(n_chain));
         }
-        // ---- epilogue: l = l_half0 + l_half1, O / l -> bf16 (each half its 64 columns)
-        if (wg == 1) {
-            sm.fin_l[r] = st.l_run;
-            sm.fin_cov[r] = st.cov;
+        // ---- epilogue: l and coverage over the four threads of a row, O / l -> bf16
+        float lt[2];
+        int ct[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            lt[k] = st.l[k] + __shfl_xor_sync(0xffffffffu, st.l[k], 1);
+            lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
+            ct[k] = st.cov[k] + __shfl_xor_sync(0xffffffffu, st.cov[k], 1);
+            ct[k] += __shfl_xor_sync(0xffffffffu, ct[k], 2);
         }
-        named_bar_sync(bar_id, 64);
-        float l_tot = st.l_run;
-        int cov_tot = st.cov;
-        if (wg == 0) {
-            l_tot += sm.fin_l[r];
-            cov_tot += sm.fin_cov[r];
-        }
-        named_bar_sync(bar_id, 64);
-        if (wg == 0) sm.fin_l[r] = l_tot; // one sum, used by both halves
-        named_bar_sync(bar_id, 64);
-        if (wg == 1) l_tot = sm.fin_l[r];
         if (ntiles > 0) {
             const int last = ntiles - 1;
             mbar_wait(&sm.pv_done[last & 1], (last >> 1) & 1);
             tc_fence_after();
         }
-        const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
-        __nv_bfloat16 *dst =
-            out + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim + 64 * wg;
+        const float inv0 = lt[0] > 0.0f ? 1.0f / lt[0] : 0.0f;
+        const float inv1 = lt[1] > 0.0f ? 1.0f / lt[1] : 0.0f;
+        __nv_bfloat16 *dst0 = out + ((static_cast<int64_t>(b) * tokens + grow0) * hq + h) * kHeadDim;
+        __nv_bfloat16 *dst1 = dst0 + 8LL * hq * kHeadDim;
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
             uint32_t o[32];
             if (ntiles > 0) {
-                tmem_ld32(oAddr + 32 * cc, o);
+                tmem_ld16x256_x8(oAddr + 64 * cc, o);
                 tmem_ld_wait();
             } else {
 #pragma unroll
                 for (int e = 0; e < 32; ++e) o[e] = 0u;
             }
-            if (row_ok) {
-                uint4 w[4];
-                uint32_t *wp = reinterpret_cast<uint32_t *>(w);
 #pragma unroll
-                for (int e = 0; e < 16; ++e)
-                    wp[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-                uint4 *d4 = reinterpret_cast<uint4 *>(dst + 32 * cc);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) d4[e] = w[e];
+            for (int R = 0; R < 8; ++R) {
+                const int col = 64 * cc + 8 * R + 2 * q4;
+                if (ok0)
+                    *reinterpret_cast<uint32_t *>(dst0 + col) =
+                        pack_bf16x2(__uint_as_float(o[4 * R]) * inv0, __uint_as_float(o[4 * R + 1]) * inv0);
+                if (ok1)
+                    *reinterpret_cast<uint32_t *>(dst1 + col) =
+                        pack_bf16x2(__uint_as_float(o[4 * R + 2]) * inv1, __uint_as_float(o[4 * R + 3]) * inv1);
             }
         }
-        if (wg == 0 && row_ok && coverage)
-            coverage[(static_cast<int64_t>(b) * hq + h) * tokens + grow] = cov_tot;
+        if (q4 == 0 && coverage) {
+            int32_t *cv = coverage + (static_cast<int64_t>(b) * hq + h) * tokens;
+            if (ok0) cv[grow0] = ct[0];
+            if (ok1) cv[grow1] = ct[1];
+        }
         if (prof) atomicAdd(&g_attn_prof[10], static_cast<unsigned long long>(clock64() - t_epi));
     }
     tc_fence_before();

@@ -348,6 +348,35 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         : "memory");
 }
 
+// 16-lane shapes (a warp may address lanes [0,16) or [16,32) of its quadrant).
+// 16x256b.x8: 16 lanes x 64 columns; thread T holds lanes T/4 and T/4+8 at
+// columns 8R + 2(T%4) + e: r[4R + 2*(second lane) + e], R < 8, e < 2.
+__device__ __forceinline__ void tmem_ld16x256_x8(uint32_t taddr, uint32_t *r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : SALE_R16(r, 0), SALE_R16(r, 16)
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16x256_x8(uint32_t taddr, const uint32_t *r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+            taddr),
+        SALE_W16(r, 0), SALE_W16(r, 16)
+        : "memory");
+}
+// 16x128b.x16: 16 lanes x 64 columns; thread T holds lanes T/4 and T/4+8 at
+// column 4R + T%4: r[2R + (second lane)], R < 16.
+__device__ __forceinline__ void tmem_st16x128_x16(uint32_t taddr, const uint32_t *r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x128b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+            taddr),
+        SALE_W16(r, 0), SALE_W16(r, 16)
+        : "memory");
+}
+
 // ------------------------------------------------------------- descriptors
 // UMMA shared-memory descriptor, SWIZZLE_128B (cute::UMMA::SmemDescriptor,
 // version 1 for sm_100). lbo/sbo in bytes.

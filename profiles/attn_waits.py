@@ -32,6 +32,5 @@ for name, m in (("sparse", mask), ("dense", None)):
           f"S wait {c[1]/t:.0f}, softmax_part {c[2]/t:.0f}; MMA per tile: loop {c[4]/t:.0f}, "
           f"K wait {c[5]/t:.0f}, P wait {c[6]/t:.0f}, V wait {c[7]/t:.0f}; epilogue/CTA "
           f"{c[10]/max(c[8],1):.0f} cyc")
-    if any(c[11:16]):
-        print("   softmax_part phases per tile: ld S %.0f, mask+max %.0f, max exchange %.0f, exp %.0f, P store %.0f"
-              % tuple(x / t for x in c[11:16]))
+    if c[12]:
+        print(f"   chain: P_(j-2) seen by the MMA issuer -> S_j seen by warp 3: {c[11]/c[12]:.0f} cyc")
