@@ -9,9 +9,12 @@
 // fully-future mask bits are ignored; coverage[g] counts the attended tokens.
 //
 // CTA = one query block i (64 tokens) of TWO query heads of the same GQA group
-// (rows 0-63 head 2p, rows 64-127 head 2p+1): both halves need exactly the same
-// K/V and the same causal extent, and per-head masks of one query block
-// overlap more than masks of adjacent query blocks (profiles/mask_stats.py).
+// as one M=128 tile: both heads need exactly the same K/V and the same causal
+// extent, and per-head masks of one query block overlap more than masks of
+// adjacent query blocks (profiles/mask_stats.py). TMEM lane 32q + 16hh + t
+// holds row 16q + t of head 2p + hh, so every lane quadrant (SMSP) has rows of
+// both heads and a tile selected by one head only keeps one of the two softmax
+// warps of every SMSP busy.
 // Key tiles follow the segment grid of the Selection-Pass: tile 0 = the
 // 32-key sink block, tile s+1 = keys [32+128s, 160+128s) = key blocks
 // 1+4s..4+4s. A tile is visited iff any of its 8 (head, kblock) bits is set;
@@ -24,13 +27,16 @@
 // and P overwrites S in place as the A operand of O += P V.
 //
 // Pipeline (warp-specialised, one elected thread per role):
-//   warp 0  TMA: K_j, V_j into a 3-stage ring (SW128 tiles)
-//   warp 1  MMA: S_j = Q K_j^T into TMEM buffer j%2 (8 x K=16), then
-//           O += P_{j-1} V_{j-1}
-//   warps 4-7  softmax, thread = row: Q row -> TMEM once; per tile tcgen05.ld S
-//           row, mask, lazy-rescaled online softmax in the exp2 domain (O
-//           rescaled in TMEM only when the running max grows by > 8),
-//           P -> bf16 -> tcgen05.st over S.
+//   warp 0  TMA: K_j (released by S_j) and V_j (released by PV_j) into 3-stage
+//           rings (SW128 tiles), K one tile ahead of V
+//   warp 1  MMA: S_0, S_1, then per tile j: O += P_j V_j, S_{j+2} = Q K^T
+//           into the buffer P_j came from
+//   warps 3-10 softmax: warp (quadrant q, index w) owns TMEM lanes 32q + 16w +
+//           [0, 16) (head 2p + w), two rows x 64 columns per thread through
+//           16x256b loads; row max by two shuffles (no cross-warp barrier);
+//           lazy-rescaled online softmax in the exp2 domain (O rescaled in
+//           TMEM only when the running max grows by > 8); P -> bf16 ->
+//           tcgen05.st over S.
 #include "common.cuh"
 
 namespace sale_b200 {
@@ -475,22 +481,23 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         }
     } else if (warp >= 3) {
         // ------------------------------------------------------------ softmax
-        const int wg = (warp - 3) >> 2;          // column half of every tile
+        // TMEM lane L = 32 quad + 16 hh + t holds row 16 quad + t of head hA + hh:
+        // both heads have rows in every lane quadrant, so a tile selected by one
+        // head only keeps one softmax warp busy on every SMSP.
+        const int wg = (warp - 3) >> 2;          // second index of the warp in its quadrant
         const int quad = warp & 3;               // TMEM lane quadrant (warp id % 4)
-        const int r = quad * 32 + lane;
-        const int half = r >> 6;                 // 0: head hA, 1: head hA + 1
-        const int h = hA + half;
-        const int64_t grow = q0 + (r & 63);
-        const bool row_ok = grow < tokens && (half == 0 || hasB);
-        const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        // Q row half -> TMEM columns [kColQ + 32 wg, +32): the A operand of S = Q K^T
+        // Q staging: thread = TMEM lane 32 quad + lane, column half wg
         {
+            const int hh = lane >> 4;
+            const int64_t qrow = q0 + quad * 16 + (lane & 15);
+            const bool q_ok = qrow < tokens && (hh == 0 || hasB);
+            const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
             uint32_t a[32];
             const uint4 *src = reinterpret_cast<const uint4 *>(
-                q + ((static_cast<int64_t>(b) * tokens + grow) * hq + h) * kHeadDim + 64 * wg);
+                q + ((static_cast<int64_t>(b) * tokens + qrow) * hq + hA + hh) * kHeadDim + 64 * wg);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const uint4 w = row_ok ? __ldg(src + e) : make_uint4(0, 0, 0, 0);
+                const uint4 w = q_ok ? __ldg(src + e) : make_uint4(0, 0, 0, 0);
                 a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
             }
             tmem_st32(lane_addr + kColQ + 32 * wg, a);
@@ -499,11 +506,14 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.q_ready);
         }
-        // softmax rows: warp (quad, wg) owns TMEM lanes quad*32 + 16 wg + [0, 16);
-        // thread rows rr0 = that + lane/4 and rr1 = rr0 + 8 (same head)
+        // softmax rows: warp (quad, wg) owns TMEM lanes 32 quad + 16 wg + [0, 16)
+        // = rows 16 quad + [0, 16) of head hA + wg; thread rows rr0 = 16 quad +
+        // lane/4 and rr1 = rr0 + 8
+        const int half = wg;
+        const int h = hA + half;
         const int q4 = lane & 3;
-        const int rr0 = quad * 32 + 16 * wg + (lane >> 2);
-        const int64_t grow0 = q0 + (rr0 & 63), grow1 = grow0 + 8;
+        const int rr0 = quad * 16 + (lane >> 2);
+        const int64_t grow0 = q0 + rr0, grow1 = grow0 + 8;
         const bool ok0 = grow0 < tokens && (half == 0 || hasB);
         const bool ok1 = grow1 < tokens && (half == 0 || hasB);
         const uint32_t lane16 = tmem + (static_cast<uint32_t>(quad * 32 + 16 * wg) << 16);
