@@ -50,3 +50,13 @@ for tau in (0.004, 0.016, 0.064):
           f"{pair_tiles / dense_pairs:.4f} of dense pair tiles; q-block-pair overhead "
           f"{2 * pair_tiles / single:.3f}x; head-pair overhead {2 * hp / single:.3f}x; "
           f"4-head union overhead {4 * h4 / single:.3f}x")
+    # best of the three head pairings of each GQA group of four, per q-block
+    if seg.shape[0] % 4 == 0:
+        best = 0
+        for g in range(seg.shape[0] // 4):
+            s4 = seg[4 * g:4 * g + 4]                       # [4, nq, ns+1]
+            opts = []
+            for (a, b), (c, d) in (((0, 1), (2, 3)), ((0, 2), (1, 3)), ((0, 3), (1, 2))):
+                opts.append((s4[a] | s4[b]).sum(-1) + (s4[c] | s4[d]).sum(-1))  # per q-block
+            best += np.minimum(np.minimum(opts[0], opts[1]), opts[2]).sum()
+        print(f"   best-of-3 head pairing per q-block overhead {2 * best / single:.3f}x")

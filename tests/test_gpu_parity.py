@@ -243,6 +243,28 @@ def test_sparse_attention_random_masks(torch):
         np.testing.assert_array_equal(cov[b, h], rcov)
 
 
+@pytest.mark.parametrize("N,Hq,Hkv", [(1, 2, 1), (31, 3, 1), (65, 2, 2), (191, 4, 1), (193, 3, 1)])
+def test_tiny_and_ragged_lengths(torch, N, Hq, Hkv):
+    """Whole prefill at lengths around the block edges (one token, a partial
+    sink block, a ragged second query block, the first query block with a
+    middle region) and odd group sizes (a head pair with one head): masks
+    bit-exact, output and coverage against the oracle on the same mask."""
+    inp = Inputs("sink_local", 21, 1, N, Hq, Hkv)
+    cells, _ = _check_selection(inp, [0.004 + 0.01 * h for h in range(Hq)])
+    q, k, v = inp.torch()
+    mask = torch.from_numpy(sale.pack_mask(cells, inp.N).view(np.int32)).cuda()
+    out, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True)
+    ref = _oracle_attention(inp, cells, inp.heads())
+    out, cov = _to_np(out.float()), _to_np(cov)
+    for (b, h), (o, rcov, st) in ref.items():
+        got = out[b, :, h, :inp.d]
+        assert max_abs(got, o) < ATOL_MAX and mean_abs(got, o) < ATOL_MEAN
+        np.testing.assert_array_equal(cov[b, h], rcov)
+    taus = [0.004 + 0.01 * h for h in range(Hq)]
+    np.testing.assert_array_equal(_to_np(sale.prefill(q, k, v, taus).view(torch.int16)),
+                                  _to_np(sale.block_sparse_attention(q, k, v, mask).view(torch.int16)))
+
+
 # ------------------------------------------------------------- accounting
 
 def test_flop_count(torch):
