@@ -311,6 +311,22 @@ std::vector<int64_t> chunk_bounds(int64_t nq, int chunks) {
     return b;
 }
 
+// Long sequences: 15 chunks, short at both ends (the first chunk's H2D and the
+// last chunk's D2H are the exposed copies) and sized in between so that each
+// chunk's H2D stays under the previous chunk's (causal, growing) compute.
+std::vector<int64_t> chunk_bounds_long(int64_t nq) {
+    static const double kFrac[] = {0.03, 0.07, 0.12, 0.18, 0.25, 0.33, 0.42, 0.52,
+                                   0.62, 0.72, 0.82, 0.90, 0.95, 0.98};
+    std::vector<int64_t> b(1, 0);
+    for (double f : kFrac) {
+        int64_t x = static_cast<int64_t>(f * static_cast<double>(nq));
+        x |= 1; // odd
+        if (x > b.back() && x < nq) b.push_back(x);
+    }
+    b.push_back(nq);
+    return b;
+}
+
 // Estimator units grouped by chunk (tile m belongs to the chunk holding query
 // block 2m+1), each group ordered like the global table.
 int ensure_chunk_units(sale_b200_ctx *ctx, int64_t tokens, const std::vector<int64_t> &bounds,
@@ -628,8 +644,8 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
     // reads data of its own and earlier chunks (causal), so the result is
     // bit-identical to the one-shot sale_b200_prefill.
     const int64_t nq = cdiv(N, kBlockQ);
-    const int chunks = N >= 16384 ? 8 : (N >= 2048 ? 4 : 1);
-    const std::vector<int64_t> bounds = chunk_bounds(nq, chunks);
+    const std::vector<int64_t> bounds =
+        N >= 65536 ? chunk_bounds_long(nq) : chunk_bounds(nq, N >= 16384 ? 8 : (N >= 2048 ? 4 : 1));
     const size_t nch = bounds.size() - 1;
     Workspace w;
     if ((st = ensure_workspace(ctx, s, &w))) return st;

@@ -299,10 +299,10 @@ def test_prefill_matches_stages_and_host_path(torch):
     np.testing.assert_array_equal(host_out, _to_np(out.view(torch.int16)).view(np.uint16))
 
 
-@pytest.mark.parametrize("B,N,Hq,Hkv", [(1, 16384, 8, 2), (2, 20000, 4, 1), (3, 3000, 7, 1)])
+@pytest.mark.parametrize("B,N,Hq,Hkv", [(1, 16384, 8, 2), (2, 20000, 4, 1), (3, 3000, 7, 1), (1, 65600, 4, 1)])
 def test_chunked_host_pipeline_bit_identical(torch, B, N, Hq, Hkv):
     """sale_b200_prefill_host streams token chunks through three streams (H2D /
-    kernels / D2H overlap, 8 chunks at >= 16K tokens, 4 at >= 2K); every stage
+    kernels / D2H overlap; 15 uneven chunks at >= 64K tokens, 8 at >= 16K, 4 at >= 2K); every stage
     reads only its own and earlier chunks, so the output equals the one-shot
     device prefill bit for bit (batch > 1 exercises the strided 2-D copies)."""
     inp = Inputs("sink_local", 9, B, N, Hq, Hkv)
