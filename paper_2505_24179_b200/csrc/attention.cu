@@ -43,14 +43,17 @@ namespace sale_b200 {
 
 constexpr int kAttnThreads = 352;  // 3 control warps + 2 softmax warpgroups (warps 3-10)
 constexpr int kMaxTiles = 4200;                // supports N <= 512K
-constexpr int kKvStages = 3;
+constexpr int kKvStages = 3;                   // K ring
+constexpr int kVStages = 2;                    // V ring (+ the constant ones chunk)
 constexpr int kTileBytesHalf = 128 * 64 * 2;   // 128 rows x 64 bf16 = 16 KB
-constexpr uint32_t kColO = 0, kColS0 = 128, kColQ = 384;
+constexpr uint32_t kColO = 0, kColL = 128, kColS0 = 160, kColQ = 416;
 
 struct AttnSmem {
     alignas(1024) uint8_t k[kKvStages][2][kTileBytesHalf];
-    alignas(1024) uint8_t v[kKvStages][2][kTileBytesHalf];
-    uint64_t q_ready, k_full[kKvStages], v_full[kKvStages], k_empty[kKvStages], v_empty[kKvStages];
+    // V as the B operand of O|l += P [V | 1]: N = 144 = two 64-column chunks of
+    // V and a chunk of ones (only 16 columns read) at stride kVStages x 16 KB
+    alignas(1024) uint8_t v[3][kVStages][kTileBytesHalf];
+    uint64_t q_ready, k_full[kKvStages], v_full[kVStages], k_empty[kKvStages], v_empty[kVStages];
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
     int ntiles;
@@ -126,12 +129,17 @@ __device__ __forceinline__ void rescale_o16(uint32_t oAddr, float a0, float a1, 
         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * ((e & 2) ? a1 : a0));
         tmem_st16x256_x8(oAddr + 64 * cc, o);
     }
+    uint32_t l4[4]; // the row sums l (O column kColL; columns kColL+8.. are not read)
+    tmem_ld16x256_x1(oAddr + (kColL - kColO), l4);
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) l4[e] = __float_as_uint(__uint_as_float(l4[e]) * ((e & 2) ? a1 : a0));
+    tmem_st16x256_x1(oAddr + (kColL - kColO), l4);
     tmem_st_wait();
 }
 
 struct SoftmaxState {
     float m[2] = {-INFINITY, -INFINITY}; // running max per row, exp2 domain (logit * scale_log2)
-    float l[2] = {0.0f, 0.0f};           // running sum of p over this thread's columns
     int cov[2] = {0, 0};                 // attended tokens in this thread's columns
 };
 
@@ -204,14 +212,13 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
         const bool need = st.m[k] != -INFINITY && m_new > st.m[k] + 8.0f;
         alpha[k] = need ? ex2_approx(st.m[k] - m_new) : 1.0f;
         if (st.m[k] == -INFINITY || need) st.m[k] = m_new;
-        if (need) st.l[k] *= alpha[k];
         need_any |= need;
     }
     const bool any_need = __any_sync(0xffffffffu, need_any);
     // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
     // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
     const unsigned long long sc2 = pack_f2(scale_log2, scale_log2);
-    unsigned long long nm2[2], psum2[2] = {0ull, 0ull};
+    unsigned long long nm2[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         const float neg_m = st.m[k] == -INFINITY ? 0.0f : -st.m[k];
@@ -251,7 +258,6 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
                     p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
                     p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
                 }
-                fadd2_f32(psum2[k], pack_f2(p0, p1));
                 s[2 * R + k] = pack_bf16x2(p0, p1); // in place: index 2R+k was already consumed
             }
     } else {
@@ -264,14 +270,9 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
                 ffma2_f32(x, sc2, nm2[k]); // x = x * scale + (-m), two lanes
                 const float p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
                 const float p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
-                fadd2_f32(psum2[k], pack_f2(p0, p1));
                 s[2 * R + k] = pack_bf16x2(p0, p1);
             }
     }
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-        st.l[k] += __uint_as_float(static_cast<uint32_t>(psum2[k])) +
-                   __uint_as_float(static_cast<uint32_t>(psum2[k] >> 32));
     st.cov[0] += nv0;
     st.cov[1] += nv1;
     tmem_st16x128_x16(sAddr, s);
@@ -315,8 +316,10 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         mbar_init(&sm.q_ready, 8);
         for (int s = 0; s < kKvStages; ++s) {
             mbar_init(&sm.k_full[s], 1);
-            mbar_init(&sm.v_full[s], 1);
             mbar_init(&sm.k_empty[s], 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
+            mbar_init(&sm.v_full[s], 1);
             mbar_init(&sm.v_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -328,6 +331,12 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+    {   // the ones chunk of the PV B operand (bf16 1.0), read by the tensor core
+        uint4 *ones = reinterpret_cast<uint4 *>(sm.v[2]);
+        for (int e = tid; e < kVStages * kTileBytesHalf / 16; e += kAttnThreads)
+            ones[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
 
     // ---- active tile list (block-wide stream compaction, ascending order)
     const int64_t rowbase = (static_cast<int64_t>(b) * hq + hA) * nq + i;
@@ -394,19 +403,19 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                 }
                 if (jj > 0) {
                     const int vj = jj - 1;
-                    const int st = vj % kKvStages;
+                    const int st = vj % kVStages;
                     const int key0 = key0_of(vj);
-                    mbar_wait(&sm.v_empty[st], ((vj / kKvStages) & 1) ^ 1);
+                    mbar_wait(&sm.v_empty[st], ((vj / kVStages) & 1) ^ 1);
                     mbar_expect_tx(&sm.v_full[st], 2 * kTileBytesHalf);
-                    tma_load_4d(sm.v[st][0], &tm_v, &sm.v_full[st], 0, g, key0, b);
-                    tma_load_4d(sm.v[st][1], &tm_v, &sm.v_full[st], 64, g, key0, b);
+                    tma_load_4d(sm.v[0][st], &tm_v, &sm.v_full[st], 0, g, key0, b);
+                    tma_load_4d(sm.v[1][st], &tm_v, &sm.v_full[st], 64, g, key0, b);
                 }
             }
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA
         if (elect_one() && ntiles > 0) {
-            constexpr uint32_t idesc_pv = idesc_bf16(128, 128, true);
+            constexpr uint32_t idesc_pv = idesc_bf16(128, 144, true); // O | l
             const bool prof = g_attn_prof_on != 0;
             const long long t_start = clock64();
             long long w_k = 0, w_p = 0, w_v = 0, t0 = 0;
@@ -447,13 +456,13 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             }
             for (int pj = 0; pj < ntiles; ++pj) {
                 const int nx = pj + 2;
-                const int pst = pj % kKvStages;
+                const int pst = pj % kVStages;
                 const int psb = pj & 1;
                 const int jp = static_cast<int>(sm.tiles[pj] & 0xFFFFu);
                 const int steps = jp == 0 ? 2 : 8;
                 if (nx < ntiles) wait_k(nx);
                 if (prof) t0 = clock64();
-                mbar_wait(&sm.v_full[pst], (pj / kKvStages) & 1);
+                mbar_wait(&sm.v_full[pst], (pj / kVStages) & 1);
                 if (prof) { w_v += clock64() - t0; t0 = clock64(); }
                 mbar_wait(&sm.p_full[psb], (pj >> 1) & 1);
                 if (prof) {
@@ -462,7 +471,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                     *reinterpret_cast<volatile long long *>(&sm.prof_tp[pj & 3]) = tn;
                 }
                 tc_fence_after();
-                const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[pst][0]), kTileBytesHalf, 1024);
+                const uint64_t vd = umma_desc_sw128(smem_u32(sm.v[0][pst]), kVStages * kTileBytesHalf, 1024);
                 const uint32_t aP = tmem + kColS0 + 128u * static_cast<uint32_t>(psb);
                 for (int kk = 0; kk < steps; ++kk)
                     mma_bf16_ts(tmem + kColO, aP + 8 * kk, vd + 128 * kk, // +16 keys = 2 KB
@@ -560,20 +569,24 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             atomicAdd(&g_attn_prof[11], static_cast<unsigned long long>(w_chain));
             atomicAdd(&g_attn_prof[12], static_cast<unsigned long long>(n_chain));
         }
-        // ---- epilogue: l and coverage over the four threads of a row, O / l -> bf16
-        float lt[2];
+        // ---- epilogue: coverage over the four threads of a row; l = the ones
+        //      column of O | l; O / l -> bf16
         int ct[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            lt[k] = st.l[k] + __shfl_xor_sync(0xffffffffu, st.l[k], 1);
-            lt[k] += __shfl_xor_sync(0xffffffffu, lt[k], 2);
             ct[k] = st.cov[k] + __shfl_xor_sync(0xffffffffu, st.cov[k], 1);
             ct[k] += __shfl_xor_sync(0xffffffffu, ct[k], 2);
         }
+        float lt[2] = {0.0f, 0.0f};
         if (ntiles > 0) {
             const int last = ntiles - 1;
             mbar_wait(&sm.pv_done[last & 1], (last >> 1) & 1);
             tc_fence_after();
+            uint32_t l4[4];
+            tmem_ld16x256_x1(oAddr + (kColL - kColO), l4);
+            tmem_ld_wait();
+            lt[0] = __uint_as_float(l4[0]);
+            lt[1] = __uint_as_float(l4[2]);
         }
         const float inv0 = lt[0] > 0.0f ? 1.0f / lt[0] : 0.0f;
         const float inv1 = lt[1] > 0.0f ? 1.0f / lt[1] : 0.0f;

@@ -377,6 +377,19 @@ __device__ __forceinline__ void tmem_st16x128_x16(uint32_t taddr, const uint32_t
         : "memory");
 }
 
+// 16x256b.x1: 16 lanes x 8 columns, thread T: lanes T/4, T/4+8 at columns
+// 2(T%4) + e: r[2 * (second lane) + e].
+__device__ __forceinline__ void tmem_ld16x256_x1(uint32_t taddr, uint32_t *r) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16x256_x1(uint32_t taddr, const uint32_t *r) {
+    asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+                 : "memory");
+}
+
 // ------------------------------------------------------------- descriptors
 // UMMA shared-memory descriptor, SWIZZLE_128B (cute::UMMA::SmemDescriptor,
 // version 1 for sm_100). lbo/sbo in bytes.
