@@ -20,6 +20,7 @@
 // padded to 272 B (68 words: at most 2-way bank conflicts for the 16 key rows
 // a warp reads). ~75 KB smem, two CTAs per SM.
 #include "common.cuh"
+#include "exp_table.h"
 
 #include <cfloat>
 
@@ -44,12 +45,41 @@ struct StatsSmem {
     double bmax[kRows][kMaxSlBlocks];          // block max, then running max
     double bsum[kRows][kMaxSlBlocks];          // per-block exp sums
     int blk_len[kMaxSlBlocks];
+    double2 exp_tab[256];                      // {hi, lo} of 2^(j/256)
 };
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
     const uint32_t d = smem_u32(dst);
     const int n = valid ? 16 : 0; // src-size 0 -> zero fill
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+
+// exp(x) for x <= 0 (the sink-local sums: logit - running max), table driven:
+// x = (256 e + j) ln2/256 + r, |r| <= ln2/512; exp(x) = 2^e 2^(j/256) e^r with
+// 2^(j/256) as a double-double from the table and e^r - 1 by a degree-5
+// polynomial; one final rounding (T_hi + fma(T_hi, q, T_lo)), i.e. within
+// ~0.5 ulp like glibc's exp (selection.hpp:155-157 uses std::exp). 11 FP64
+// operations against ~17 for the CUDA math library's exp. x < -700 returns 0
+// instead of a value below 2^-1009: every block sum is added to l >= 1 (the
+// running max element contributes exp(0) = 1), where such a term is lost in
+// the rounding anyway, so l is unchanged.
+__device__ __forceinline__ double exp_nonpos(double x, const double2 *tab) {
+    const bool tiny = x < -700.0;
+    x = tiny ? -700.0 : x;
+    const double t = fma(x, 369.32993046757463, 6755399441055744.0); // 256/ln2, 1.5 * 2^52
+    const int k = __double2loint(t);
+    const double kd = t - 6755399441055744.0;
+    double r = fma(kd, -2.7076061740622863e-03, x);  // ln2/256, hi
+    r = fma(kd, -9.058776616587108e-20, r);          // ln2/256, lo
+    double q = fma(r, 8.3333333333333332e-03, 4.1666666666666664e-02);
+    q = fma(q, r, 1.6666666666666666e-01);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    q = q * r;                                       // e^r - 1
+    const double2 tj = tab[k & 255];
+    const double y = tj.x + fma(tj.x, q, tj.y);
+    const double v = __hiloint2double(__double2hiint(y) + ((k >> 8) << 20), __double2loint(y));
+    return tiny ? 0.0 : v;
 }
 
 __device__ __forceinline__ void ffma2(unsigned long long &acc, unsigned long long a,
@@ -117,6 +147,8 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     auto slot_token = [&](int slot) -> int64_t {
         return slot == 0 ? 0 : (2 * i - 4 + slot - 1) * kBlockK;
     };
+    for (int e = tid; e < 256; e += kThreads)
+        sm.exp_tab[e] = make_double2(c_exp2_256[2 * e], c_exp2_256[2 * e + 1]);
     if (tid < kMaxSlBlocks) {
         int len = 0;
         if (tid < nsl) {
@@ -265,13 +297,13 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
             for (int t0 = 0; t0 < kBlockK; t0 += 8) {
                 double e[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t) e[t] = exp(static_cast<double>(lg[t0 + t]) - m_new);
+                for (int t = 0; t < 8; ++t) e[t] = exp_nonpos(static_cast<double>(lg[t0 + t]) - m_new, sm.exp_tab);
 #pragma unroll
                 for (int t = 0; t < 8; ++t) sum = __dadd_rn(sum, e[t]);
             }
         } else {
             for (int t = 0; t < sm.blk_len[s]; ++t)
-                sum = __dadd_rn(sum, exp(static_cast<double>(lg[t]) - m_new));
+                sum = __dadd_rn(sum, exp_nonpos(static_cast<double>(lg[t]) - m_new, sm.exp_tab));
         }
         sm.bsum[r][s] = sum;
     }
@@ -284,7 +316,7 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         double l = 0.0, m_old = -INFINITY;
         for (int s = 0; s < nsl; ++s) {
             const double m_new = sm.bmax[r][s];
-            l = __dadd_rn(__dmul_rn(l, exp(m_old - m_new)), sm.bsum[r][s]);
+            l = __dadd_rn(__dmul_rn(l, exp_nonpos(m_old - m_new, sm.exp_tab)), sm.bsum[r][s]);
             m_old = m_new;
         }
         double scaled = __dmul_rn(taus[h], l);

@@ -117,7 +117,7 @@ def _check_selection(inp, taus, dbg_check=True):
             continue
         est = ~np.isnan(rdbg["m"])
         np.testing.assert_array_equal(m[b, h][est], rdbg["m"][est])
-        # exp_sum: CUDA double exp (<=1 ulp) vs glibc -> allow 2 ulp
+        # exp_sum: table-driven double exp (~0.5 ulp) vs glibc -> allow 2 ulp
         np.testing.assert_allclose(l[b, h][est], rdbg["l"][est], rtol=4.5e-16, atol=0)
         np.testing.assert_allclose(bound[b, h][est], rdbg["bound"][est], rtol=1e-15, atol=1e-15)
         # the B200 path estimates the full segments only: the trailing partial
