@@ -18,20 +18,45 @@ namespace sale_b200 {
 
 namespace {
 
-// Code of one element, returned as its int8 bit pattern in the low byte. All
-// float arithmetic (FMA / ALU pipes): no float<->int conversions, which run on
-// the quarter-rate XU pipe.
-__device__ __forceinline__ uint32_t quantize_one(float x, float scale, float inv_scale) {
+// Code of one element as a float in [-7, 7] (exact integer). All float
+// arithmetic on the FMA / ALU pipes, no branches and no float<->int
+// conversions (quarter-rate XU pipe). k0 = rint(a * inv) is within one of the
+// exact code (inv is only approximately 1/scale); the two fmaf signs decide
+// the exact half-away-from-zero rounding: a < (k0 - 1/2) scale -> k0 - 1,
+// a >= (k0 + 1/2) scale -> k0 + 1 (a single rounding of an exact value cannot
+// change its sign). k0 = 0 never steps down (the bound is negative) and k0 = 7
+// never steps up (a <= peak < 7.5 scale), so no clamps are needed.
+__device__ __forceinline__ float set_le0(float v) {
+    float r;
+    asm("set.le.f32.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(v));
+    return r;
+}
+__device__ __forceinline__ float set_gt0(float v) {
+    float r;
+    asm("set.gt.f32.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(v));
+    return r;
+}
+__device__ __forceinline__ float quantize_one(float x, float scale, float inv_scale) {
     constexpr float kMagic = 12582912.0f; // 1.5 * 2^23: x + kMagic rounds x to an integer
     const float a = fabsf(x);
-    float k = fminf((a * inv_scale + kMagic) - kMagic, 7.0f); // within one of the exact code
-    // exact corrections: a < (k - 1/2) * scale -> k - 1; a >= (k + 1/2) * scale
-    // -> k + 1 (ties go away from zero); the fmaf sign is exact
-    const bool down = k > 0.0f && fmaf(2.0f * k - 1.0f, scale, -2.0f * a) > 0.0f;
-    const bool up = k < 7.0f && fmaf(2.0f * k + 1.0f, scale, -2.0f * a) <= 0.0f;
-    k += up ? 1.0f : (down ? -1.0f : 0.0f);
-    // integer -7..7 -> two's complement byte in the low mantissa bits
-    return static_cast<uint32_t>(__float_as_int((x < 0.0f ? -k : k) + kMagic)) & 0xFFu;
+    const float k0 = fmaf(a, inv_scale, kMagic) - kMagic;
+    const float dn = set_gt0(fmaf(k0 - 0.5f, scale, -a)); // k0 -+ 1/2 are exact
+    const float up = set_le0(fmaf(k0 + 0.5f, scale, -a));
+    const float k = (k0 + up) - dn;
+    return __uint_as_float(__float_as_uint(k) | (__float_as_uint(x) & 0x80000000u));
+}
+
+// Codes as floats -> eight int8 bytes: c + kMagic holds the two's complement
+// integer in its low mantissa bits; PRMT gathers the low bytes.
+__device__ __forceinline__ uint2 pack8f(const float (&c)[8]) {
+    constexpr float kMagic = 12582912.0f;
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = __float_as_uint(c[i] + kMagic);
+    uint2 r;
+    r.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+    r.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
+    return r;
 }
 
 __device__ __forceinline__ void unpack8(const uint4 &u, float (&f)[8]) {
@@ -43,20 +68,20 @@ __device__ __forceinline__ void unpack8(const uint4 &u, float (&f)[8]) {
     }
 }
 
-__device__ __forceinline__ uint2 pack8(const uint32_t (&c)[8]) {
-    uint2 r;
-    r.x = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-    r.y = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
-    return r;
-}
-
 __device__ __forceinline__ float scale_of(float peak) {
     return peak > 0.0f ? __fdiv_rn(peak, 7.0f) : 1.0f;
 }
+// An approximate 1/scale is enough (k0 only has to be within one); scales
+// below 2^-100 are handled by exact power-of-two rescaling of a and scale.
+__device__ __forceinline__ float rcp_approx(float v) {
+    float r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
 
 constexpr int kThreads = 256;
-constexpr int kLanesPerRow = 16;  // Q: 16 lanes x 8 elements per 128-wide row
-constexpr int kQSlots = 4;        // Q rows per 16-lane group in flight (4 x 16 B loads per thread)
+constexpr int kLanesPerRow = 8;   // Q: 8 lanes x 16 elements per 128-wide row
+constexpr int kQSlots = 2;        // Q rows per 8-lane group in flight (2 x 2 x 16 B loads per thread)
 constexpr int kQRowsPerCta = kThreads / kLanesPerRow * kQSlots; // 64
 
 // CTAs [0, q_ctas): 64 consecutive Q rows ((b, n, h) order), every thread
@@ -71,46 +96,66 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
                    int64_t t_hi) {
     const int tid = threadIdx.x;
     if (blockIdx.x < q_ctas) {
-        // local Q rows (b, n in [t_lo, t_hi), h) -> global rows (b*N + n)*Hq + h
-        const int64_t span_rows = (t_hi - t_lo) * hq;
-        const int64_t q_rows = batch * span_rows;
+        // local Q rows (b, n in [t_lo, t_hi), h) -> global rows (b*N + n)*Hq + h,
+        // all in 32-bit arithmetic (batch * tokens * hq < 2^31 is checked at
+        // launch); the whole-sequence case is the identity map.
+        const uint32_t hq32 = static_cast<uint32_t>(hq), n32 = static_cast<uint32_t>(tokens);
+        const uint32_t span = static_cast<uint32_t>((t_hi - t_lo) * hq);
+        const uint32_t q_rows = static_cast<uint32_t>(batch) * span;
+        const bool whole = t_lo == 0 && t_hi == tokens;
+        const uint32_t lo_rows = static_cast<uint32_t>(t_lo) * hq32, n_rows = n32 * hq32;
         const int sub = tid % kLanesPerRow;
-        const int64_t loc0 = static_cast<int64_t>(blockIdx.x) * kQRowsPerCta + tid / kLanesPerRow;
-        auto global_row = [&](int64_t loc) {
-            const int64_t b = loc / span_rows;
-            return (b * tokens + t_lo) * hq + (loc - b * span_rows);
-        };
-        uint4 u[kQSlots];
+        const uint32_t loc0 = blockIdx.x * static_cast<uint32_t>(kQRowsPerCta) + tid / kLanesPerRow;
+        uint32_t row[kQSlots];
+        uint4 u[kQSlots][2];
 #pragma unroll
         for (int sl = 0; sl < kQSlots; ++sl) {
-            const int64_t loc = loc0 + sl * (kThreads / kLanesPerRow);
-            u[sl] = loc < q_rows ? __ldcs(reinterpret_cast<const uint4 *>(q + global_row(loc) * kHeadDim) + sub)
-                                 : make_uint4(0, 0, 0, 0);
+            const uint32_t loc = loc0 + sl * (kThreads / kLanesPerRow);
+            uint32_t rr = loc;
+            if (!whole) {
+                const uint32_t bb = loc / span;
+                rr = bb * n_rows + lo_rows + (loc - bb * span);
+            }
+            row[sl] = loc < q_rows ? rr : 0xFFFFFFFFu;
+            const uint4 *src = reinterpret_cast<const uint4 *>(q + static_cast<int64_t>(rr) * kHeadDim) + 2 * sub;
+            u[sl][0] = loc < q_rows ? __ldcs(src) : make_uint4(0, 0, 0, 0);
+            u[sl][1] = loc < q_rows ? __ldcs(src + 1) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int sl = 0; sl < kQSlots; ++sl) {
-            const int64_t loc = loc0 + sl * (kThreads / kLanesPerRow);
-            const int64_t row = loc < q_rows ? global_row(loc) : 0;
-            float f[8];
-            unpack8(u[sl], f);
+            float f0[8], f1[8];
+            unpack8(u[sl][0], f0);
+            unpack8(u[sl][1], f1);
             float peak = 0.0f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) peak = fmaxf(peak, fabsf(f[i]));
+            for (int i = 0; i < 8; ++i) peak = fmaxf(peak, fmaxf(fabsf(f0[i]), fabsf(f1[i])));
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
-            if (loc >= q_rows) continue;
+            for (int o = 4; o > 0; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+            if (row[sl] == 0xFFFFFFFFu) continue;
             const float scale = scale_of(peak);
-            const float inv = 1.0f / scale;
-            uint32_t c[8];
+            float sc = scale;
+            if (scale < 7.8886091e-31f) { // 2^-100: rescale exactly by 2^64
 #pragma unroll
-            for (int i = 0; i < 8; ++i) c[i] = quantize_one(f[i], scale, inv);
-            __stcs(reinterpret_cast<uint2 *>(q_codes + row * kHeadDim) + sub, pack8(c));
+                for (int i = 0; i < 8; ++i) {
+                    f0[i] *= 18446744073709551616.0f;
+                    f1[i] *= 18446744073709551616.0f;
+                }
+                sc *= 18446744073709551616.0f;
+            }
+            const float inv = rcp_approx(sc);
+            float c0[8], c1[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                c0[i] = quantize_one(f0[i], sc, inv);
+                c1[i] = quantize_one(f1[i], sc, inv);
+            }
+            uint2 *dst = reinterpret_cast<uint2 *>(q_codes + static_cast<int64_t>(row[sl]) * kHeadDim) + 2 * sub;
+            __stcs(dst, pack8f(c0));
+            __stcs(dst + 1, pack8f(c1));
             if (sub == 0) {
                 // row = (b*N + n)*Hq + h  ->  scales[b][h][n]
-                const uint32_t r32 = static_cast<uint32_t>(row), hq32 = static_cast<uint32_t>(hq);
-                const uint32_t h = r32 % hq32, bn = r32 / hq32;
-                const uint32_t n32 = static_cast<uint32_t>(tokens);
-                const uint32_t b = bn / n32, n = bn % n32;
+                const uint32_t h = row[sl] % hq32, bn = row[sl] / hq32;
+                const uint32_t b = bn / n32, n = bn - b * n32;
                 q_scales[(static_cast<int64_t>(b) * hq + h) * tokens + n] = scale;
             }
         }
@@ -148,17 +193,26 @@ quantize_qk_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__r
 #pragma unroll
     for (int w = 1; w < kThreads / 32; ++w) peak = fmaxf(peak, warp_peak[w]);
     const float scale = scale_of(peak);
-    const float inv = 1.0f / scale;
     if (valid) {
-        uint32_t c0[8], c1[8];
+        float sc = scale;
+        if (scale < 7.8886091e-31f) { // 2^-100: rescale exactly by 2^64
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                f0[i] *= 18446744073709551616.0f;
+                f1[i] *= 18446744073709551616.0f;
+            }
+            sc *= 18446744073709551616.0f;
+        }
+        const float inv = rcp_approx(sc);
+        float c0[8], c1[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            c0[i] = quantize_one(f0[i], scale, inv);
-            c1[i] = quantize_one(f1[i], scale, inv);
+            c0[i] = quantize_one(f0[i], sc, inv);
+            c1[i] = quantize_one(f1[i], sc, inv);
         }
         uint2 *dst = reinterpret_cast<uint2 *>(k_codes + row * kHeadDim) + sub;
-        __stcs(dst, pack8(c0));
-        __stcs(dst + 1, pack8(c1));
+        __stcs(dst, pack8f(c0));
+        __stcs(dst + 1, pack8f(c1));
     }
     if (tid == 0) k_scales[(b * hkv + h) * nk + j] = scale;
 }

@@ -280,6 +280,33 @@ def test_flop_count(torch):
             assert tuple(counts[b, h]) == (r["computed"], r["skipped"], r["total"])
 
 
+def test_quantize_ties_and_tiny_groups(torch):
+    """Exact half-away ties ((k + 1/2) * scale with scale a power of two) and
+    groups whose scale is subnormal (the kernel's exact 2^64 rescaling path),
+    per token (Q) and per 32-token block (K), against the C oracle."""
+    rng = np.random.default_rng(3)
+    N = 64
+    x = np.zeros((1, N, 2, 128), np.float32)
+    for n in range(N):
+        for h in range(2):
+            e = [-3, -131, 5, -126][(n + h) % 4]
+            ties = (rng.integers(-7, 7, 128) + 0.5) * 2.0 ** e
+            row = np.where(rng.random(128) < 0.5, ties, rng.normal(0, 4, 128) * 2.0 ** e)
+            row[0] = 7 * 2.0 ** e                          # peak -> scale 2^e exactly
+            x[0, n, h] = np.clip(row, -7 * 2.0 ** e, 7 * 2.0 ** e)
+    xt = torch.from_numpy(x).to(torch.bfloat16)
+    xb = xt.float().numpy()                                # the bf16 values the kernel sees
+    qc, qs = (_to_np(t) for t in sale.quantize_per_token(xt.cuda()))
+    kc, ks = (_to_np(t) for t in sale.quantize_per_key_block(xt.cuda()))
+    for h in range(2):
+        codes, scales = O.quantize(np.ascontiguousarray(xb[0, :, h]), 1)
+        np.testing.assert_array_equal(qc[0, :, h], codes)
+        np.testing.assert_array_equal(qs[0, h], scales)
+        codes, scales = O.quantize(np.ascontiguousarray(xb[0, :, h]), 32)
+        np.testing.assert_array_equal(kc[0, :, h], codes)
+        np.testing.assert_array_equal(ks[0, h], scales)
+
+
 # -------------------------------------------------------------- pipeline
 
 def test_prefill_matches_stages_and_host_path(torch):
