@@ -67,7 +67,7 @@ struct AttnSmem {
 // lane 0, summed over CTAs); [4] MMA loop total, [5] K waits, [6] P waits,
 // [7] V waits, [8] CTAs, [9] prologue (start -> tile list ready, thread 0),
 // [10] epilogue (last tile -> end, warp 3 lane 0).
-__device__ int g_attn_prof_on = 0;
+bool g_attn_prof_host = false; // host: launch the kProf instance
 __device__ unsigned long long g_attn_prof[16];
 
 namespace {
@@ -280,6 +280,9 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
     if (any_need) rescale_o16(oAddr, alpha[0], alpha[1], pv_prev, pv_parity);
 }
 
+// kProf: the cycle-instrumented instance (sale_b200_attention_profile); the
+// production instance carries no profiling code.
+template <bool kProf>
 __global__ void __launch_bounds__(kAttnThreads, 1)
 sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const uint32_t *__restrict__ mask,
@@ -287,6 +290,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                         int64_t tokens, int hq, int hkv, float scale_log2, int64_t i_lo,
                         int64_t ni) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const long long t_kernel = clock64();
     AttnSmem &sm = *reinterpret_cast<AttnSmem *>(smem_raw + smem_pad_1k(smem_raw));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -301,10 +305,14 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
     // HBM about once and then served from L2.
     const int group = hq / hkv;
     const int npairs = (group + 1) / 2;
-    const int p = static_cast<int>(blockIdx.x % npairs);
+    // 32-bit index math (grid < 2^31; ni <= nq)
+    const uint32_t bx = blockIdx.x, np32 = static_cast<uint32_t>(npairs), ni32 = static_cast<uint32_t>(ni);
+    const uint32_t bq = bx / np32;
+    const int p = static_cast<int>(bx - bq * np32);
     // query blocks [i_lo, i_lo + ni): a token-range slice (chunked host pipeline)
-    const int64_t i = i_lo + ni - 1 - static_cast<int64_t>((blockIdx.x / npairs) % ni);
-    const int bg = static_cast<int>(blockIdx.x / (npairs * ni));
+    const uint32_t bgq = bq / ni32;
+    const int64_t i = i_lo + ni - 1 - static_cast<int64_t>(bq - bgq * ni32);
+    const int bg = static_cast<int>(bgq);
     const int g = bg % hkv;
     const int b = bg / hkv;
     const int hA = g * group + 2 * p;
@@ -327,57 +335,104 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             mbar_init(&sm.p_full[s], 8);
             mbar_init(&sm.pv_done[s], 1);
         }
-        sm.ntiles = 0;
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
-    {   // the ones chunk of the PV B operand (bf16 1.0), read by the tensor core
+    if (warp == 2) {
+        tmem_alloc<512>(&sm.tmem_base);
+        if (lane == 0 && kProf)
+            atomicAdd(&g_attn_prof[13], static_cast<unsigned long long>(clock64() - t_kernel));
+    } else if (warp == 3) {
+        // ---- active tile list (ascending), built by this warp while the
+        // others set up: lane t of a pass owns the 8 segment tiles 8t+1 ..
+        // 8t+8 = key blocks 32t+1 .. 32t+32 (bits 1-31 of mask word t, bit 0
+        // of word t+1); tile 0 is the sink block. The words of four passes are
+        // loaded before any is used (one memory round trip per 1024 tiles).
+        const int64_t rowbase = (static_cast<int64_t>(b) * hq + hA) * nq + i;
+        const uint32_t *rowA = mask ? mask + rowbase * words : nullptr;
+        const uint32_t *rowB = (mask && hasB) ? mask + (rowbase + nq) * words : nullptr;
+        const int total = qend > kBlockK ? 1 + static_cast<int>((qend - kBlockK + 127) / 128) : 1;
+        const int64_t jmax = min(nk, (qend + kBlockK - 1) / kBlockK) - 1; // last causal key block
+        const int groups = (total - 1 + 7) / 8;
+        auto word = [&](const uint32_t *row, int64_t t) -> uint32_t {
+            return !row ? 0xFFFFFFFFu : (t < words ? row[t] : 0u);
+        };
+        const uint32_t a0 = mask ? rowA[0] & 1u : 1u;
+        const uint32_t b0 = !hasB ? 0u : (mask ? rowB[0] & 1u : 1u);
+        uint32_t wa[5], wb[5]; // words t, t+32, t+64, t+96 and t+128 (for the last bit)
+        auto load_pass = [&](int start) {
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const int64_t t = start + 32 * u + lane;
+                wa[u] = word(rowA, t);
+                wb[u] = hasB ? word(rowB, t) : 0u;
+            }
+        };
+        if (lane == 0 && kProf)
+            atomicAdd(&g_attn_prof[12], static_cast<unsigned long long>(clock64() - t_kernel));
+        load_pass(0);
+        const uint32_t sink = a0 | (b0 << 4);
+        int carry = sink ? 1 : 0;
+        if (lane == 0 && sink) sm.tiles[0] = sink << 16;
+        for (int start = 0; start < groups; start += 128) {
+            if (start > 0) load_pass(start);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = start + 32 * u + lane;
+                // bit 0 of word t+1: lane+1's word, or the next pass's lane 0
+                const uint32_t na = __shfl_down_sync(0xffffffffu, wa[u], 1);
+                const uint32_t nb = __shfl_down_sync(0xffffffffu, wb[u], 1);
+                const uint32_t ha = __shfl_sync(0xffffffffu, wa[u + 1], 0);
+                const uint32_t hb = __shfl_sync(0xffffffffu, wb[u + 1], 0);
+                if (start + 32 * u >= groups) break; // warp-uniform: nothing left
+                uint32_t xa = 0, xb = 0;
+                if (t < groups) {
+                    const int64_t avail = jmax - 32LL * t; // blocks 32t+1 .. 32t+avail are causal
+                    const uint32_t cm = avail >= 32 ? 0xFFFFFFFFu : (avail <= 0 ? 0u : (1u << avail) - 1u);
+                    xa = ((wa[u] >> 1) | ((lane == 31 ? ha : na) << 31)) & cm;
+                    xb = hasB ? ((wb[u] >> 1) | ((lane == 31 ? hb : nb) << 31)) & cm : 0u;
+                }
+                uint32_t act = 0; // bit e: tile 8t+1+e active
+#pragma unroll
+                for (int e = 0; e < 8; ++e) act |= (((xa | xb) >> (4 * e)) & 0xFu) ? (1u << e) : 0u;
+                // exclusive warp prefix of the counts (<= 8, four bits) by ballots
+                const int c = __popc(act);
+                const uint32_t lt = (1u << lane) - 1u;
+                int excl = 0, tot = 0;
+#pragma unroll
+                for (int bit = 0; bit < 4; ++bit) {
+                    const uint32_t m = __ballot_sync(0xffffffffu, (c >> bit) & 1);
+                    excl += __popc(m & lt) << bit;
+                    tot += __popc(m) << bit;
+                }
+                int pos = carry + excl;
+                while (act) {
+                    const int e = __ffs(act) - 1;
+                    act &= act - 1;
+                    const uint32_t bits = ((xa >> (4 * e)) & 0xFu) | (((xb >> (4 * e)) & 0xFu) << 4);
+                    if (pos < kMaxTiles) sm.tiles[pos] = static_cast<uint32_t>(8 * t + 1 + e) | (bits << 16);
+                    ++pos;
+                }
+                carry += tot;
+            }
+        }
+        if (lane == 0) sm.ntiles = carry < kMaxTiles ? carry : kMaxTiles;
+        if (lane == 0 && kProf)
+            atomicAdd(&g_attn_prof[14], static_cast<unsigned long long>(clock64() - t_kernel));
+    } else {
+        // the ones chunk of the PV B operand (bf16 1.0), read by the tensor core
         uint4 *ones = reinterpret_cast<uint4 *>(sm.v[2]);
-        for (int e = tid; e < kVStages * kTileBytesHalf / 16; e += kAttnThreads)
+        const int t2 = tid < 64 ? tid : tid - 64; // threads other than warps 2, 3
+        for (int e = t2; e < kVStages * kTileBytesHalf / 16; e += kAttnThreads - 64)
             ones[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-
-    // ---- active tile list (block-wide stream compaction, ascending order)
-    const int64_t rowbase = (static_cast<int64_t>(b) * hq + hA) * nq + i;
-    const uint32_t *rowA = mask ? mask + rowbase * words : nullptr;
-    const uint32_t *rowB = (mask && hasB) ? mask + (rowbase + nq) * words : nullptr;
-    const int total = qend > kBlockK ? 1 + static_cast<int>((qend - kBlockK + 127) / 128) : 1;
-    __syncthreads();
-    for (int start = 0; start < total; start += kAttnThreads) {
-        const int j = start + tid;
-        uint32_t bits = 0;
-        if (j < total) {
-            const int64_t j0 = j == 0 ? 0 : 1 + 4LL * (j - 1);
-            const int nsub = j == 0 ? 1 : 4;
-            uint32_t causal = 0; // key blocks that exist and are not fully future
-            for (int e = 0; e < nsub; ++e)
-                if (j0 + e < nk && (j0 + e) * kBlockK < qend) causal |= 1u << e;
-            const uint32_t nibA = mask ? mask_bits4(rowA, words, j0) : 0xFu;
-            const uint32_t nibB = !hasB ? 0u : (mask ? mask_bits4(rowB, words, j0) : 0xFu);
-            bits = (nibA & causal) | ((nibB & causal) << 4);
-        }
-        const bool active = bits != 0;
-        const uint32_t ballot = __ballot_sync(0xffffffffu, active);
-        if (lane == 0) sm.warp_cnt[warp] = __popc(ballot);
-        __syncthreads();
-        int base = sm.ntiles;
-        for (int w = 0; w < warp; ++w) base += sm.warp_cnt[w];
-        if (active) {
-            const int pos = base + __popc(ballot & ((1u << lane) - 1u));
-            if (pos < kMaxTiles) sm.tiles[pos] = static_cast<uint32_t>(j) | (bits << 16);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            int s = sm.ntiles;
-            for (int w = 0; w < kAttnThreads / 32; ++w) s += sm.warp_cnt[w];
-            sm.ntiles = s < kMaxTiles ? s : kMaxTiles;
-        }
-        __syncthreads();
+        if (tid == 0 && kProf)
+            atomicAdd(&g_attn_prof[15], static_cast<unsigned long long>(clock64() - t_kernel));
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (threadIdx.x == 0 && kProf)
+        atomicAdd(&g_attn_prof[9], static_cast<unsigned long long>(clock64() - t_kernel));
     const uint32_t tmem = sm.tmem_base;
     const int ntiles = sm.ntiles;
 
@@ -416,7 +471,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         // ---------------------------------------------------------------- MMA
         if (elect_one() && ntiles > 0) {
             constexpr uint32_t idesc_pv = idesc_bf16(128, 144, true); // O | l
-            const bool prof = g_attn_prof_on != 0;
+            const bool prof = kProf;
             const long long t_start = clock64();
             long long w_k = 0, w_p = 0, w_v = 0, t0 = 0;
             mbar_wait(&sm.q_ready, 0);
@@ -528,7 +583,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         const uint32_t lane16 = tmem + (static_cast<uint32_t>(quad * 32 + 16 * wg) << 16);
         SoftmaxState st;
         const uint32_t oAddr = lane16 + kColO;
-        const bool prof = warp == 3 && lane == 0 && g_attn_prof_on != 0;
+        const bool prof = warp == 3 && lane == 0 && kProf;
         const long long t_loop = clock64();
         long long w_s = 0, t_part = 0, t1 = 0, w_chain = 0, n_chain = 0;
         for (int jj = 0; jj < ntiles; ++jj) {
@@ -567,7 +622,6 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             atomicAdd(&g_attn_prof[2], static_cast<unsigned long long>(t_part));
             atomicAdd(&g_attn_prof[3], static_cast<unsigned long long>(ntiles));
             atomicAdd(&g_attn_prof[11], static_cast<unsigned long long>(w_chain));
-            atomicAdd(&g_attn_prof[12], static_cast<unsigned long long>(n_chain));
         }
         // ---- epilogue: coverage over the four threads of a row; l = the ones
         //      column of O | l; O / l -> bf16
@@ -638,7 +692,8 @@ cudaError_t attention_profile(int enable, unsigned long long *out16) {
     unsigned long long zero[16] = {};
     cudaError_t e = cudaMemcpyToSymbol(g_attn_prof, zero, sizeof(zero));
     if (e != cudaSuccess) return e;
-    return cudaMemcpyToSymbol(g_attn_prof_on, &enable, sizeof(int));
+    g_attn_prof_host = enable != 0;
+    return cudaSuccess;
 }
 
 size_t attention_smem_bytes() { return sizeof(AttnSmem) + 1024; }
@@ -652,17 +707,19 @@ cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, cons
     static bool configured = false;
     const size_t smem = attention_smem_bytes();
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(sparse_attention_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
+        for (auto kern : {sparse_attention_kernel<false>, sparse_attention_kernel<true>}) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
         configured = true;
     }
     const int npairs = (hq / hkv + 1) / 2;
     if (i_hi < 0 || i_hi > nq) i_hi = nq;
     if (i_hi <= i_lo) return cudaSuccess;
     const int64_t grid = batch * hkv * npairs * (i_hi - i_lo);
-    sparse_attention_kernel<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
+    auto kern = g_attn_prof_host ? sparse_attention_kernel<true> : sparse_attention_kernel<false>;
+    kern<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
         static_cast<const __nv_bfloat16 *>(q), tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out),
         coverage, tokens, hq, hkv, scale_log2, i_lo, i_hi - i_lo);
     return cudaGetLastError();

@@ -21,7 +21,12 @@ sale.prefill(q, k, v, 0.004, mask_out=mask)
 ctx = sale.context()
 lib = ctx.lib
 lib.sale_b200_attention_profile.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
-for name, m in (("sparse", mask), ("dense", None)):
+mask64 = None
+if len(sys.argv) > 2:  # a second tau: its mask as a third case
+    mask64 = torch.empty_like(mask)
+    sale.prefill(q, k, v, float(sys.argv[2]), mask_out=mask64)
+cases = [("sparse", mask), ("dense", None)] + ([("sparse tau " + sys.argv[2], mask64)] if mask64 is not None else [])
+for name, m in cases:
     cnt = (C.c_uint64 * 16)()
     lib.sale_b200_attention_profile(ctx.handle, 1, None)
     sale.block_sparse_attention(q, k, v, m)
@@ -31,6 +36,7 @@ for name, m in (("sparse", mask), ("dense", None)):
     print(f"[{name}] tiles/CTA {c[3]/max(c[8],1):.0f}; softmax warp per tile: loop {c[0]/t:.0f} cyc, "
           f"S wait {c[1]/t:.0f}, softmax_part {c[2]/t:.0f}; MMA per tile: loop {c[4]/t:.0f}, "
           f"K wait {c[5]/t:.0f}, P wait {c[6]/t:.0f}, V wait {c[7]/t:.0f}; epilogue/CTA "
-          f"{c[10]/max(c[8],1):.0f} cyc")
-    if c[12]:
-        print(f"   chain: P_(j-2) seen by the MMA issuer -> S_j seen by warp 3: {c[11]/c[12]:.0f} cyc")
+          f"{c[10]/max(c[8],1):.0f} cyc; prologue/CTA {c[9]/max(c[8],1):.0f} cyc "
+          f"(list warp start {c[12]/max(c[8],1):.0f}, TMEM alloc done {c[13]/max(c[8],1):.0f}, tile list done {c[14]/max(c[8],1):.0f}, "
+          f"barrier init + ones done {c[15]/max(c[8],1):.0f})")
+
