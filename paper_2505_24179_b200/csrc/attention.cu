@@ -21,20 +21,23 @@
 // inside a visited tile unselected 32-key sub-blocks and the causal diagonal
 // are masked per row.
 //
-// TMEM (512 columns): O [0,128) | S0 [128,256) | S1 [256,384) | Q [384,448).
+// TMEM (512 columns): O | l [0,144) | S0 [160,288) | S1 [288,416) | Q [416,480).
 // Q sits in TMEM as the A operand of S = Q K^T (only K streams from shared
 // memory; with A in SMEM an M=N=128 bf16 MMA needs the full 128 B/clk port),
-// and P overwrites S in place as the A operand of O += P V.
+// and P overwrites S in place as the A operand of O | l += P [V | 1]: the
+// N = 144 PV MMA also produces the row sums l from a constant ones chunk.
 //
 // Pipeline (warp-specialised, one elected thread per role):
-//   warp 0  TMA: K_j (released by S_j) and V_j (released by PV_j) into 3-stage
-//           rings (SW128 tiles), K one tile ahead of V
-//   warp 1  MMA: S_0, S_1, then per tile j: O += P_j V_j, S_{j+2} = Q K^T
-//           into the buffer P_j came from
+//   warp 0  TMA: K_j (released by S_j) and V_j (released by PV_j) into 3- / 2-
+//           stage rings (SW128 tiles), K one tile ahead of V
+//   warp 1  MMA: S_0, S_1, then per tile j: O | l += P_j [V_j | 1], S_{j+2} =
+//           Q K^T into the buffer P_j came from
+//   warp 2  TMEM allocator; warp 3 also builds the active tile list while the
+//           others initialise barriers and the ones chunk
 //   warps 3-10 softmax: warp (quadrant q, index w) owns TMEM lanes 32q + 16w +
 //           [0, 16) (head 2p + w), two rows x 64 columns per thread through
 //           16x256b loads; row max by two shuffles (no cross-warp barrier);
-//           lazy-rescaled online softmax in the exp2 domain (O rescaled in
+//           lazy-rescaled online softmax in the exp2 domain (O | l rescaled in
 //           TMEM only when the running max grows by > 8); P -> bf16 ->
 //           tcgen05.st over S.
 #include "common.cuh"
@@ -57,7 +60,6 @@ struct AttnSmem {
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
     int ntiles;
-    int warp_cnt[kAttnThreads / 32];
     long long prof_tp[4];      // profiling: MMA-side time P_j was observed (ring)
     uint32_t tiles[kMaxTiles]; // j | bits8 << 16
 };
@@ -66,20 +68,13 @@ struct AttnSmem {
 // loop total, [1] S-ready waits, [2] softmax_part time, [3] tiles (warp 3,
 // lane 0, summed over CTAs); [4] MMA loop total, [5] K waits, [6] P waits,
 // [7] V waits, [8] CTAs, [9] prologue (start -> tile list ready, thread 0),
-// [10] epilogue (last tile -> end, warp 3 lane 0).
+// [10] epilogue (last tile -> end, warp 3 lane 0), [11] MMA-side P -> S chain,
+// [12] tile-list warp start, [13] TMEM allocated, [14] tile list done,
+// [15] barriers + ones chunk done.
 bool g_attn_prof_host = false; // host: launch the kProf instance
 __device__ unsigned long long g_attn_prof[16];
 
 namespace {
-
-__device__ __forceinline__ uint32_t mask_bits4(const uint32_t *row, int64_t words, int64_t j0) {
-    // bits j0 .. j0+3 of a packed mask row
-    const int64_t w = j0 >> 5;
-    const int sh = static_cast<int>(j0 & 31);
-    uint64_t v = row[w];
-    if (w + 1 < words) v |= static_cast<uint64_t>(row[w + 1]) << 32;
-    return static_cast<uint32_t>(v >> sh) & 0xFu;
-}
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float r;
