@@ -60,6 +60,7 @@ struct AttnSmem {
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
     int ntiles;
+    int warp_tot[8];           // tile-list build: per-warp counts of a round
     long long prof_tp[4];      // profiling: MMA-side time P_j was observed (ring)
     uint32_t tiles[kMaxTiles]; // j | bits8 << 16
 };
@@ -336,12 +337,15 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         tmem_alloc<512>(&sm.tmem_base);
         if (lane == 0 && kProf)
             atomicAdd(&g_attn_prof[13], static_cast<unsigned long long>(clock64() - t_kernel));
-    } else if (warp == 3) {
-        // ---- active tile list (ascending), built by this warp while the
-        // others set up: lane t of a pass owns the 8 segment tiles 8t+1 ..
-        // 8t+8 = key blocks 32t+1 .. 32t+32 (bits 1-31 of mask word t, bit 0
-        // of word t+1); tile 0 is the sink block. The words of four passes are
-        // loaded before any is used (one memory round trip per 1024 tiles).
+    } else if (warp >= 3) {
+        // ---- active tile list (ascending), built by the 8 softmax warps while
+        // the control warps set up: per round, warp w3 = warp - 3 takes pass
+        // p = 8 round + w3 = segment-tile groups [32p, 32p + 32); lane t of a
+        // pass owns the 8 tiles 8g+1 .. 8g+8 (g = 32p + t) = key blocks
+        // 32g+1 .. 32g+32 (bits 1-31 of mask word g, bit 0 of word g+1); tile
+        // 0 is the sink block. Prefix sums: ballots within a warp, the eight
+        // warp totals through shared memory (one named barrier per round).
+        const int w3 = warp - 3;
         const int64_t rowbase = (static_cast<int64_t>(b) * hq + hA) * nq + i;
         const uint32_t *rowA = mask ? mask + rowbase * words : nullptr;
         const uint32_t *rowB = (mask && hasB) ? mask + (rowbase + nq) * words : nullptr;
@@ -353,71 +357,59 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         };
         const uint32_t a0 = mask ? rowA[0] & 1u : 1u;
         const uint32_t b0 = !hasB ? 0u : (mask ? rowB[0] & 1u : 1u);
-        uint32_t wa[5], wb[5]; // words t, t+32, t+64, t+96 and t+128 (for the last bit)
-        auto load_pass = [&](int start) {
-#pragma unroll
-            for (int u = 0; u < 5; ++u) {
-                const int64_t t = start + 32 * u + lane;
-                wa[u] = word(rowA, t);
-                wb[u] = hasB ? word(rowB, t) : 0u;
-            }
-        };
-        if (lane == 0 && kProf)
-            atomicAdd(&g_attn_prof[12], static_cast<unsigned long long>(clock64() - t_kernel));
-        load_pass(0);
         const uint32_t sink = a0 | (b0 << 4);
         int carry = sink ? 1 : 0;
-        if (lane == 0 && sink) sm.tiles[0] = sink << 16;
-        for (int start = 0; start < groups; start += 128) {
-            if (start > 0) load_pass(start);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = start + 32 * u + lane;
-                // bit 0 of word t+1: lane+1's word, or the next pass's lane 0
-                const uint32_t na = __shfl_down_sync(0xffffffffu, wa[u], 1);
-                const uint32_t nb = __shfl_down_sync(0xffffffffu, wb[u], 1);
-                const uint32_t ha = __shfl_sync(0xffffffffu, wa[u + 1], 0);
-                const uint32_t hb = __shfl_sync(0xffffffffu, wb[u + 1], 0);
-                if (start + 32 * u >= groups) break; // warp-uniform: nothing left
-                uint32_t xa = 0, xb = 0;
-                if (t < groups) {
-                    const int64_t avail = jmax - 32LL * t; // blocks 32t+1 .. 32t+avail are causal
-                    const uint32_t cm = avail >= 32 ? 0xFFFFFFFFu : (avail <= 0 ? 0u : (1u << avail) - 1u);
-                    xa = ((wa[u] >> 1) | ((lane == 31 ? ha : na) << 31)) & cm;
-                    xb = hasB ? ((wb[u] >> 1) | ((lane == 31 ? hb : nb) << 31)) & cm : 0u;
-                }
-                uint32_t act = 0; // bit e: tile 8t+1+e active
-#pragma unroll
-                for (int e = 0; e < 8; ++e) act |= (((xa | xb) >> (4 * e)) & 0xFu) ? (1u << e) : 0u;
-                // exclusive warp prefix of the counts (<= 8, four bits) by ballots
-                const int c = __popc(act);
-                const uint32_t lt = (1u << lane) - 1u;
-                int excl = 0, tot = 0;
-#pragma unroll
-                for (int bit = 0; bit < 4; ++bit) {
-                    const uint32_t m = __ballot_sync(0xffffffffu, (c >> bit) & 1);
-                    excl += __popc(m & lt) << bit;
-                    tot += __popc(m) << bit;
-                }
-                int pos = carry + excl;
-                while (act) {
-                    const int e = __ffs(act) - 1;
-                    act &= act - 1;
-                    const uint32_t bits = ((xa >> (4 * e)) & 0xFu) | (((xb >> (4 * e)) & 0xFu) << 4);
-                    if (pos < kMaxTiles) sm.tiles[pos] = static_cast<uint32_t>(8 * t + 1 + e) | (bits << 16);
-                    ++pos;
-                }
-                carry += tot;
+        if (tid == 96 && sink) sm.tiles[0] = sink << 16;
+        const uint32_t lt = (1u << lane) - 1u;
+        for (int base = 0; base < groups; base += 256) {
+            const int t = base + 32 * w3 + lane; // this lane's group
+            uint32_t xa = 0, xb = 0;
+            if (t < groups) {
+                const uint32_t wa = word(rowA, t), wa1 = word(rowA, t + 1);
+                const uint32_t wb = hasB ? word(rowB, t) : 0u, wb1 = hasB ? word(rowB, t + 1) : 0u;
+                const int64_t avail = jmax - 32LL * t; // blocks 32t+1 .. 32t+avail are causal
+                const uint32_t cm = avail >= 32 ? 0xFFFFFFFFu : (avail <= 0 ? 0u : (1u << avail) - 1u);
+                xa = ((wa >> 1) | (wa1 << 31)) & cm;
+                xb = ((wb >> 1) | (wb1 << 31)) & cm;
             }
+            uint32_t act = 0; // bit e: tile 8t+1+e active
+#pragma unroll
+            for (int e = 0; e < 8; ++e) act |= (((xa | xb) >> (4 * e)) & 0xFu) ? (1u << e) : 0u;
+            const int c = __popc(act);
+            int excl = 0, tot = 0;
+#pragma unroll
+            for (int bit = 0; bit < 4; ++bit) {
+                const uint32_t m = __ballot_sync(0xffffffffu, (c >> bit) & 1);
+                excl += __popc(m & lt) << bit;
+                tot += __popc(m) << bit;
+            }
+            if (lane == 0) sm.warp_tot[w3] = tot;
+            named_bar_sync(1, 256);
+            int before = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const int x = sm.warp_tot[w];
+                before += w < w3 ? x : 0;
+                all += x;
+            }
+            int pos = carry + before + excl;
+            while (act) {
+                const int e = __ffs(act) - 1;
+                act &= act - 1;
+                const uint32_t bits = ((xa >> (4 * e)) & 0xFu) | (((xb >> (4 * e)) & 0xFu) << 4);
+                if (pos < kMaxTiles) sm.tiles[pos] = static_cast<uint32_t>(8 * t + 1 + e) | (bits << 16);
+                ++pos;
+            }
+            carry += all;
+            named_bar_sync(1, 256); // warp_tot is reused by the next round
         }
-        if (lane == 0) sm.ntiles = carry < kMaxTiles ? carry : kMaxTiles;
-        if (lane == 0 && kProf)
+        if (tid == 96) sm.ntiles = carry < kMaxTiles ? carry : kMaxTiles;
+        if (tid == 96 && kProf)
             atomicAdd(&g_attn_prof[14], static_cast<unsigned long long>(clock64() - t_kernel));
     } else {
         // the ones chunk of the PV B operand (bf16 1.0), read by the tensor core
         uint4 *ones = reinterpret_cast<uint4 *>(sm.v[2]);
-        const int t2 = tid < 64 ? tid : tid - 64; // threads other than warps 2, 3
-        for (int e = t2; e < kVStages * kTileBytesHalf / 16; e += kAttnThreads - 64)
+        for (int e = tid; e < kVStages * kTileBytesHalf / 16; e += 64) // warps 0, 1
             ones[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (tid == 0 && kProf)
