@@ -129,10 +129,10 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
-// Arrive on an mbarrier of CTA `rank` (possibly this CTA), cluster scope.
+// Arrive on an mbarrier of CTA `rank` (possibly this CTA). Default (CTA-scope
+// release) semantics: the .release.cluster form adds a MEMBAR.GPU per arrive.
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t *bar, uint32_t rank) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                     mapa_shared(smem_u32(bar), rank))
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(smem_u32(bar), rank))
                  : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
@@ -233,6 +233,50 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t cta_mask) {
         "h"(cta_mask)
         : "memory");
 }
+// ---- CTA pairs (cta_group::2, a cluster of two CTAs on one TPC)
+// TMA into this CTA's shared memory, completing bytes on the LEADER CTA's
+// mbarrier at the same offset (peer bit cleared).
+__device__ __forceinline__ void tma_load_4d_2sm(void *smem_dst, const void *tmap, uint64_t *bar,
+                                                int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+template <uint32_t kCols> __device__ __forceinline__ void tmem_alloc_2sm(uint32_t *dst_smem) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols> __device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+                 : "memory");
+}
+// Pair MMA (issued by the leader CTA): M = 256 rows, A rows 0-127 from the
+// leader's shared memory and 128-255 from the peer's (same descriptor), B split
+// along N between the two CTAs; D rows 0-127 in the leader's TMEM, 128-255 in
+// the peer's (same column address).
+__device__ __forceinline__ void mma_i8_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Arrive on the barrier at this offset in every CTA of cta_mask once the pair
+// MMAs issued so far have completed.
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t *bar, uint16_t cta_mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
+}
+
 // D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32
 __device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                           uint32_t idesc, uint32_t accumulate) {
