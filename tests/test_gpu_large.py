@@ -123,3 +123,33 @@ def test_tau_monotone_and_dense_identity_128k(torch):
     a = sale.block_sparse_attention(q, k, v, ones)
     b = sale.block_sparse_attention(q, k, v, None)
     assert torch.equal(a, b)
+
+
+def test_long_sequence_300k_sampled(torch):
+    """Beyond 256K tokens the attention kernel's tile lists take several
+    build rounds (> 2048 key tiles per query block) and the estimator several
+    units per query tile: sampled masks and rows against the oracle, and the
+    all-ones mask against the dense run bit for bit."""
+    N, tau = 300032, 0.016
+    inp = Inputs("sink_local", 5, 1, N, 2, 1)
+    q, k, v = inp.torch()
+    nq, nk, nw = sale.grid(N)
+    mask = torch.empty((1, 2, nq, nw), dtype=torch.int32, device="cuda")
+    out = sale.prefill(q, k, v, tau, mask_out=mask)
+    cells = sale.unpack_mask(_np(mask), N)
+    outf = _np(out.float())
+    rng = np.random.default_rng(3)
+    for h in (0, 1):
+        qh, kh, vh = inp.qh(0, h), inp.kh(0, 0), inp.vh(0, 0)
+        qc, qs = O.quantize(qh, 1)
+        kc, ks = O.quantize(kh, 32)
+        for i in sorted(set([3, nq - 1] + list(rng.integers(3, nq, 3)))):
+            ref = oracle_mask_row(qh, kh, qc, qs, kc, ks, int(i), tau, N)
+            np.testing.assert_array_equal(cells[0, h, i], ref, err_msg=f"h={h} i={i}")
+        rows = sorted(set([0, N - 1] + list(rng.integers(N // 2, N, 10))))
+        ref = sampled_attention(qh, kh, vh, cells[0, h], rows)
+        err = np.abs(outf[0, rows, h, :128] - ref)
+        assert err.max() < 2e-2 and err.mean() < 1e-3, (h, err.max(), err.mean())
+    ones = torch.full_like(mask, -1)
+    dense = sale.block_sparse_attention(q, k, v, None)
+    assert torch.equal(sale.block_sparse_attention(q, k, v, ones), dense)
