@@ -160,8 +160,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
         tmem_st_wait();
         return;
     }
-    tmem_ld16x256_x8(sAddr, s);
-    tmem_ld16x256_x8(sAddr + 64, s + 32);
+    tmem_ld16x256_x16(sAddr, s);
     tmem_ld_wait();
     const bool full = nib == 0xFu && lim0 >= 127 && lim1 >= 127;
     int nv0 = 64, nv1 = 64;

@@ -402,6 +402,16 @@ __device__ __forceinline__ void tmem_ld16x256_x8(uint32_t taddr, uint32_t *r) {
         : SALE_R16(r, 0), SALE_R16(r, 16)
         : "r"(taddr));
 }
+// 16x256b.x16: 16 lanes x 128 columns, r[4R + 2*(second lane) + e], R < 16.
+__device__ __forceinline__ void tmem_ld16x256_x16(uint32_t taddr, uint32_t *r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,"
+        "%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,"
+        "%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : SALE_R16(r, 0), SALE_R16(r, 16), SALE_R16(r, 32), SALE_R16(r, 48)
+        : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st16x256_x8(uint32_t taddr, const uint32_t *r) {
     asm volatile(
         "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
