@@ -345,19 +345,24 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
 __global__ void base_mask_kernel(uint32_t *__restrict__ mask, int64_t rows, int64_t nq,
                                  int64_t nk, int64_t words, int64_t tokens, int64_t i_lo,
                                  int64_t ni) {
-    const int64_t loc = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (loc >= rows * ni * words) return;
-    const int64_t w = loc % words;
-    const int64_t i = i_lo + (loc / words) % ni;
-    const int64_t bh = loc / (words * ni);
-    const int64_t idx = (bh * nq + i) * words + w;
+    // one thread per word; 32-bit index math (rows * ni * words < 2^31 is
+    // checked at launch), the word's bits from the row's range by two shifts
+    const uint32_t loc = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t w32 = static_cast<uint32_t>(words), ni32 = static_cast<uint32_t>(ni);
+    if (loc >= static_cast<uint32_t>(rows) * ni32 * w32) return;
+    const uint32_t rw = loc / w32;
+    const int64_t w = loc - rw * w32;
+    const uint32_t bh = rw / ni32;
+    const int64_t i = i_lo + (rw - bh * ni32);
+    const int64_t idx = (static_cast<int64_t>(bh) * nq + i) * words + w;
     const int64_t fr = frontier_block(i, tokens, nk);
     const int64_t lo = i >= 3 ? 1 + kSegment * full_segments(i) : 0;
+    const int64_t a = lo > 32 * w ? lo : 32 * w, bnd = fr < 32 * w + 31 ? fr : 32 * w + 31;
     uint32_t bits = 0;
-    for (int e = 0; e < 32; ++e) {
-        const int64_t j = w * 32 + e;
-        if (j == 0 || (j >= lo && j <= fr)) bits |= 1u << e;
-    }
+    if (a <= bnd)
+        bits = (0xFFFFFFFFu >> (31 - static_cast<int>(bnd - 32 * w))) &
+               (0xFFFFFFFFu << static_cast<int>(a - 32 * w));
+    if (w == 0) bits |= 1u; // the sink block
     mask[idx] = bits;
 }
 
@@ -396,6 +401,7 @@ cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t 
     if (i_hi < 0 || i_hi > nq) i_hi = nq;
     if (i_hi <= i_lo) return cudaSuccess;
     const int64_t total = batch * hq * (i_hi - i_lo) * words;
+    if (total > 0x7FFFFFFF) return cudaErrorInvalidValue;
     const int threads = 256;
     const int64_t blocks = (total + threads - 1) / threads;
     base_mask_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
