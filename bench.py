@@ -228,16 +228,25 @@ def run_b200(a):
         # one GPU per rank; more ranks than GPUs (a functional check on a
         # single-GPU box) share devices round-robin
         torch.cuda.set_device(local % torch.cuda.device_count())
-        dist.init_process_group("nccl")
+        # NCCL needs one GPU per rank; BENCH_DIST_BACKEND=gloo runs a functional
+        # multi-rank check with several ranks on one GPU (timings not meaningful)
+        dist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
     else:
         torch.cuda.set_device(0)
     from paper_2505_24179_b200 import sale
     sale.load_library()
 
     Hq, Hkv, d = MODEL["q_heads"], MODEL["kv_heads"], MODEL["head_dim"]
-    if Hkv % world:
-        raise SystemExit(f"--gpus {world} must divide the {Hkv} KV heads")
-    hkv = Hkv // world
+    # (batch, KV group) units sharded over ranks; with fewer groups than ranks
+    # each group is split into query-block ranges over `split` ranks with K/V
+    # replicated, balanced by causal work
+    if Hkv % world == 0:
+        split, hkv, kv_begin = 1, Hkv // world, rank * (Hkv // world)
+    elif world % Hkv == 0:
+        split, hkv, kv_begin = world // Hkv, 1, rank // (world // Hkv)
+    else:
+        raise SystemExit(f"--gpus {world} must divide or be a multiple of the {Hkv} KV heads")
+    part = rank % split
     hq = hkv * (Hq // Hkv)
     B = a.batch
     threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE",
@@ -268,13 +277,14 @@ def run_b200(a):
         dense-mask run, per-stage times, density, algorithmic work. Per-rank
         values; the caller reduces over ranks."""
         q16, k16, v16 = sale.workload_gqa("sink_local", a.seed, B, N, hq, hkv, d, threads=threads,
-                                          kv_begin=rank * hkv)
+                                          kv_begin=kv_begin)
         q, k, v = dev(q16), dev(k16), dev(v16)
         taus = [a.tau] * hq
         nq, nk, nw = sale.grid(N)
-        mask = torch.empty((B, hq, nq, nw), dtype=torch.int32, device="cuda")
-        prefill = lambda: sale.prefill(q, k, v, taus, mask_out=mask)
-        dense = lambda: sale.block_sparse_attention(q, k, v, None)
+        rng = sale.query_block_split(nq, split)[part] if split > 1 else None
+        mask = torch.zeros((B, hq, nq, nw), dtype=torch.int32, device="cuda")
+        prefill = lambda: sale.prefill(q, k, v, taus, mask_out=mask, q_blocks=rng)
+        dense = lambda: sale.block_sparse_attention(q, k, v, None, q_blocks=rng)
         r = {"N": N}
         # ---- K full SALE prefills, device-timed (clocks sampled on the headline)
         if headline:
@@ -293,17 +303,26 @@ def run_b200(a):
             stages.append(sale.stage_times())
         sale.set_timing(False)
         r["stage_ms"] = {key: float(np.mean([st[key] for st in stages])) for key in stages[0]}
-        # ---- density and algorithmic work
-        counts = sale.flop_accounting(mask, N).cpu().numpy()
-        r["computed"], r["total"] = int(counts[..., 0].sum()), int(counts[..., 2].sum())
-        _, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True)
-        r["attended"] = int(cov.to(torch.int64).sum().item())
-        f_i = np.arange(nq)
+        # ---- density and algorithmic work (this rank's rows)
+        i0, i1 = rng if rng is not None else (0, nq)
+        if rng is None:
+            counts = sale.flop_accounting(mask, N).cpu().numpy()
+            r["computed"], r["total"] = int(counts[..., 0].sum()), int(counts[..., 2].sum())
+        else:
+            cells = sale.unpack_mask(mask[:, :, i0:i1].cpu().numpy(), N)  # rows i0..i1-1
+            ii = np.arange(i0, i1)[:, None]
+            causal = (32 * np.arange(nk))[None, :] < np.minimum(64 * (ii + 1), N)
+            r["computed"] = int((cells[:, :, : i1 - i0] * causal).sum())
+            r["total"] = int(B * hq * causal.sum())
+        _, cov = sale.block_sparse_attention(q, k, v, mask, coverage=True, q_blocks=rng)
+        t0, t1 = 64 * i0, min(64 * i1, N)
+        r["attended"] = int(cov[:, :, t0:t1].to(torch.int64).sum().item())
+        f_i = np.arange(i0, i1)
         r["est_blocks"] = B * hq * int(np.where(f_i >= 3, 4 * ((2 * f_i - 5) // 4), 0).sum())
         if not headline:
             return r
         # ---- optional output gather over NCCL (timed separately, max over ranks)
-        if a.gather and world > 1:
+        if a.gather and world > 1 and split == 1:
             out = prefill()
             r["gather_ms"] = timed(lambda: sale.gather_heads(out), 3, 1)
         # ---- tau sweep (density vs latency)
@@ -311,13 +330,13 @@ def run_b200(a):
         taus_sweep = [float(x) for x in a.sweep.split(",") if x.strip()] if a.sweep else []
         for t in taus_sweep:
             tt = [t] * hq
-            ms_t = timed(lambda: sale.prefill(q, k, v, tt, mask_out=mask), 3, warmup)
+            ms_t = timed(lambda: sale.prefill(q, k, v, tt, mask_out=mask, q_blocks=rng), 3, warmup)
             c = sale.flop_accounting(mask, N).cpu().numpy()
             r["sweep"].append({"tau": t, "density": float(c[..., 0].sum() / c[..., 2].sum()),
-                               "ms": ms_t})
+                               "ms": ms_t})  # (split ranks: the density of this rank's rows only)
         # ---- e2e through the public host API (pinned buffers, copies timed)
         r["e2e_ms"] = None
-        if not a.no_e2e:
+        if not a.no_e2e and split == 1:
             del q, k, v
             pin = lambda x: torch.from_numpy(x).pin_memory()
             hq16, hk16, hv16 = pin(q16), pin(k16), pin(v16)
@@ -401,12 +420,14 @@ def run_b200(a):
             "dtype": "bf16 (attention) / int8 (estimator)", "data": "synthetic",
             "config": {"workload": workload_name(a), "tokens": N, "batch": B, "tau": a.tau,
                        "q_heads": Hq, "kv_heads": Hkv, "head_dim": d,
-                       "parallelism": f"kv-group sharded x{world}, no collective",
+                       "parallelism": (f"kv-group sharded x{world}, no collective" if split == 1 else
+                                       f"{Hkv} kv groups x {split} query-block ranges (K/V "
+                                       "replicated), no collective"),
                        "l2": f"inputs ({B * N * (Hq + 2 * Hkv) * d * 2 / 2**30:.2f} GiB) larger "
                              "than L2; no flush"},
             "speedup_vs_dense": ms_dense / ms_step, "dense_ms": ms_dense,
             "estimation_overhead_pct": 100.0 * overhead, "density": density,
-            "stage_ms": stage_ms, "effective_tflops": dense_flops * world / (ms_step * 1e-3) / 1e12,
+            "stage_ms": stage_ms, "effective_tflops": dense_flops / (ms_step * 1e-3) / 1e12,
             "tau_sweep": sweep, "roofline": roof, "clocks": clock,
             "gpu_launches": 5 * a.steps}
     if "gather_ms" in main_r:

@@ -141,6 +141,20 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
                       const sale_b200_shape *shape, const double *taus,
                       const sale_b200_selection_config *cfg, void *out, uint32_t *mask_out,
                       void *stream);
+/* One query-block range [i_lo, i_hi) of sale_b200_prefill (a GPU's share when
+ * a (batch, KV group) unit is split across GPUs, K/V replicated; SURVEY.md
+ * §8(e)): writes the mask and output rows of the range only. Boundaries must
+ * be 0, nq or odd query blocks. The results of the range equal those of the
+ * whole-sequence call. */
+int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                            const sale_b200_shape *shape, const double *taus,
+                            const sale_b200_selection_config *cfg, int64_t i_lo, int64_t i_hi,
+                            void *out, uint32_t *mask_out, void *stream);
+/* sale_b200_sparse_attention restricted to query blocks [i_lo, i_hi). */
+int sale_b200_sparse_attention_range(sale_b200_ctx *ctx, const void *q, const void *k,
+                                     const void *v, const sale_b200_shape *shape,
+                                     const uint32_t *mask_words, int64_t i_lo, int64_t i_hi,
+                                     void *out, int32_t *coverage, void *stream);
 /* Same, end to end from HOST buffers (bf16 bit patterns, uint16): H2D copies,
  * the three stages and the D2H copy of out, synchronous on return. */
 int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t *k,

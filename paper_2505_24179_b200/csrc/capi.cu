@@ -282,7 +282,7 @@ int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *
 
 int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
                    const sale_b200_shape &s, const uint32_t *mask, void *out, int32_t *coverage,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1) {
     int st;
     CUtensorMap tk, tv;
     if ((st = make_map(ctx, &tk, k, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
@@ -290,7 +290,7 @@ int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void 
     const float scale_log2 = inv_sqrt_dim(s.head_dim) * 1.4426950408889634f;
     SALE_CUDA(ctx, launch_sparse_attention(q, tk, tv, mask, out, coverage, s.batch, s.tokens,
                                            static_cast<int>(s.q_heads), static_cast<int>(s.kv_heads),
-                                           scale_log2, stream));
+                                           scale_log2, stream, i_lo, i_hi));
     mark(ctx, 5, stream);
     return SALE_B200_OK;
 }
@@ -611,6 +611,87 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
                           mask, w.thresh, nullptr, s)))
         return st;
     return attention_impl(ctx, q, k, v, *shape, mask, out, nullptr, s);
+}
+
+// A query-block range [i_lo, i_hi) of the prefill (one GPU's share when a
+// (batch, KV group) is split across GPUs): K is quantized for
+// every key the range attends ([0, t_hi)), Q only for the range's rows; the
+// mask and output rows of the range are written, other rows are untouched.
+// Boundaries are 0, nq or odd (estimator tiles pair query blocks 2m+1, 2m+2).
+static int check_range(sale_b200_ctx *ctx, const sale_b200_shape *shape, int64_t i_lo, int64_t i_hi) {
+    const int64_t nq = cdiv(shape->tokens, kBlockQ);
+    if (i_lo < 0 || i_hi > nq || i_lo >= i_hi)
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT, "query-block range outside [0, nq)");
+    if ((i_lo != 0 && (i_lo & 1) == 0) || (i_hi != nq && (i_hi & 1) == 0))
+        return fail(ctx, SALE_B200_INVALID_ARGUMENT,
+                    "query-block range boundaries must be 0, nq or odd");
+    return SALE_B200_OK;
+}
+
+int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
+                            const sale_b200_shape *shape, const double *taus,
+                            const sale_b200_selection_config *cfg, int64_t i_lo, int64_t i_hi,
+                            void *out, uint32_t *mask_out, void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int st;
+    if ((st = check_shape(ctx, shape))) return st;
+    if ((st = check_config(ctx, cfg))) return st;
+    if ((st = check_taus(ctx, taus, shape->q_heads))) return st;
+    if ((st = check_range(ctx, shape, i_lo, i_hi))) return st;
+    if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    const sale_b200_shape sh = *shape;
+    const int64_t B = sh.batch, N = sh.tokens, Hq = sh.q_heads, Hkv = sh.kv_heads;
+    const int64_t nq = cdiv(N, kBlockQ);
+    Workspace w;
+    if ((st = ensure_workspace(ctx, sh, &w))) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t *mask = mask_out ? mask_out : w.mask;
+    std::vector<int64_t> bounds(1, 0);
+    if (i_lo > 0) bounds.push_back(i_lo);
+    if (i_hi < nq) bounds.push_back(i_hi);
+    bounds.push_back(nq);
+    const size_t grp = i_lo > 0 ? 1 : 0; // the unit group of [i_lo, i_hi)
+    if ((st = upload_taus(ctx, taus, Hq, s))) return st;
+    if ((st = ensure_chunk_units(ctx, N, bounds, s))) return st;
+    const int64_t t0 = i_lo * kBlockQ, t1 = std::min<int64_t>(i_hi * kBlockQ, N);
+    mark(ctx, 0, s);
+    SALE_CUDA(ctx, launch_quantize_qk(nullptr, k, nullptr, nullptr, w.k_codes, w.k_scales, B, N, Hq,
+                                      Hkv, s, 0, t1));
+    SALE_CUDA(ctx, launch_quantize_qk(q, nullptr, w.q_codes, w.q_scales, nullptr, nullptr, B, N, Hq,
+                                      Hkv, s, t0, t1));
+    mark(ctx, 1, s);
+    const float isd = inv_sqrt_dim(sh.head_dim);
+    SALE_CUDA(ctx, launch_base_mask(mask, B, Hq, N, s, i_lo, i_hi));
+    mark(ctx, 2, s);
+    SALE_CUDA(ctx, launch_sink_local_stats(q, k, B, N, Hq, Hkv, isd, ctx->d_taus, w.thresh, nullptr,
+                                           nullptr, nullptr, s, i_lo, i_hi));
+    mark(ctx, 3, s);
+    const int64_t u0 = ctx->cunit_off[grp], u1 = ctx->cunit_off[grp + 1];
+    if (u1 > u0) {
+        CUtensorMap tm_qc, tm_kc;
+        if ((st = make_map(ctx, &tm_qc, w.q_codes, false, B, N, Hq, 128, 128))) return st;
+        if ((st = make_map(ctx, &tm_kc, w.k_codes, false, B, N, Hkv, 128, 128))) return st;
+        SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_cunits + u0, u1 - u0, w.q_scales,
+                                       w.k_scales, w.thresh, mask, B, N, static_cast<int>(Hq),
+                                       static_cast<int>(Hkv), isd, nullptr, s));
+    }
+    mark(ctx, 4, s);
+    return attention_impl(ctx, q, k, v, sh, mask, out, nullptr, s, i_lo, i_hi);
+}
+
+int sale_b200_sparse_attention_range(sale_b200_ctx *ctx, const void *q, const void *k,
+                                     const void *v, const sale_b200_shape *shape,
+                                     const uint32_t *mask_words, int64_t i_lo, int64_t i_hi,
+                                     void *out, int32_t *coverage, void *stream) {
+    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    int st;
+    if ((st = check_shape(ctx, shape))) return st;
+    if ((st = check_range(ctx, shape, i_lo, i_hi))) return st;
+    if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
+    return attention_impl(ctx, q, k, v, *shape, mask_words, out, coverage,
+                          static_cast<cudaStream_t>(stream), i_lo, i_hi);
 }
 
 int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t *k,

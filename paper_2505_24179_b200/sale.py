@@ -119,6 +119,10 @@ def load_library() -> C.CDLL:
                                         P(SelectionConfig), vp, vp, vp]),
         "sale_b200_prefill_host": (C.c_int, [vp, vp, vp, vp, P(Shape), P(C.c_double),
                                              P(SelectionConfig), vp]),
+        "sale_b200_prefill_range": (C.c_int, [vp, vp, vp, vp, P(Shape), P(C.c_double),
+                                              P(SelectionConfig), i64, i64, vp, vp, vp]),
+        "sale_b200_sparse_attention_range": (C.c_int, [vp, vp, vp, vp, P(Shape), vp, i64, i64,
+                                                       vp, vp, vp]),
         "sale_b200_workload_head_f32": (C.c_int, [C.c_int, C.c_uint64, i64, i64, i64, vp, vp, vp]),
         "sale_b200_workload_gqa_bf16": (C.c_int, [C.c_int, C.c_uint64, P(Shape), vp, vp, vp,
                                                   C.c_int]),
@@ -310,19 +314,25 @@ def selection_pass(q, k, q_codes, q_scales, k_codes, k_scales, taus, head_dim=12
     return (mask, dbg) if debug else mask
 
 
-def block_sparse_attention(q, k, v, mask=None, head_dim=128, coverage=False):
+def block_sparse_attention(q, k, v, mask=None, head_dim=128, coverage=False, q_blocks=None):
     """sparse_attention.hpp:37 (mask = packed words) or, with mask=None,
     full_attention (attention.hpp:18). Returns out bf16 [B,N,Hq,128]
-    (and coverage int32 [B,Hq,N])."""
+    (and coverage int32 [B,Hq,N]). q_blocks=(i_lo, i_hi): only those query
+    blocks' rows are computed (boundaries 0, nq or odd)."""
     import torch
     ctx = context()
     s = _shape_of(q, k, head_dim)
     out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
     cov = (torch.empty((s.batch, s.q_heads, s.tokens), dtype=torch.int32, device=q.device)
            if coverage else None)
-    ctx._check(ctx.lib.sale_b200_sparse_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v),
-                                                  C.byref(s), _ptr(mask), _ptr(out), _ptr(cov),
-                                                  _stream()))
+    if q_blocks is None:
+        ctx._check(ctx.lib.sale_b200_sparse_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v),
+                                                      C.byref(s), _ptr(mask), _ptr(out),
+                                                      _ptr(cov), _stream()))
+    else:
+        ctx._check(ctx.lib.sale_b200_sparse_attention_range(
+            ctx.handle, _ptr(q), _ptr(k), _ptr(v), C.byref(s), _ptr(mask), int(q_blocks[0]),
+            int(q_blocks[1]), _ptr(out), _ptr(cov), _stream()))
     return (out, cov) if coverage else out
 
 
@@ -342,19 +352,42 @@ def flop_accounting(mask, tokens):
     return counts
 
 
-def prefill(q, k, v, taus, head_dim=128, mask_out=None, config=None):
+def prefill(q, k, v, taus, head_dim=128, mask_out=None, config=None, q_blocks=None):
     """run_pipeline's stage composition (runner.hpp:63-80) on device tensors:
-    quantize -> selection -> block-sparse attention. Returns out bf16."""
+    quantize -> selection -> block-sparse attention. Returns out bf16.
+    q_blocks=(i_lo, i_hi): only that query-block range (one GPU's share of a
+    split unit, K/V replicated); rows outside it are left untouched."""
     import torch
     ctx = context()
     s = _shape_of(q, k, head_dim)
     taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (s.q_heads,)))
     out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
     cfg = config if config is not None else default_config()
-    ctx._check(ctx.lib.sale_b200_prefill(ctx.handle, _ptr(q), _ptr(k), _ptr(v), C.byref(s),
-                                         taus.ctypes.data_as(C.POINTER(C.c_double)), C.byref(cfg),
-                                         _ptr(out), _ptr(mask_out), _stream()))
+    tp = taus.ctypes.data_as(C.POINTER(C.c_double))
+    if q_blocks is None:
+        ctx._check(ctx.lib.sale_b200_prefill(ctx.handle, _ptr(q), _ptr(k), _ptr(v), C.byref(s), tp,
+                                             C.byref(cfg), _ptr(out), _ptr(mask_out), _stream()))
+    else:
+        ctx._check(ctx.lib.sale_b200_prefill_range(ctx.handle, _ptr(q), _ptr(k), _ptr(v),
+                                                   C.byref(s), tp, C.byref(cfg),
+                                                   int(q_blocks[0]), int(q_blocks[1]), _ptr(out),
+                                                   _ptr(mask_out), _stream()))
     return out
+
+
+def query_block_split(nq, parts):
+    """Query-block ranges of one (batch, KV group) unit split across `parts`
+    GPUs (units < GPUs). The causal work of query block i
+    grows like i, so the cumulative work like i^2: boundary p sits near
+    nq * sqrt(p / parts), rounded to an odd block (the estimator pairs query
+    blocks 2m+1, 2m+2). Returns [(i_lo, i_hi), ...] covering [0, nq)."""
+    bounds = [0]
+    for p in range(1, parts):
+        x = int(round(nq * (p / parts) ** 0.5)) | 1
+        if bounds[-1] < x < nq:
+            bounds.append(x)
+    bounds.append(nq)
+    return list(zip(bounds[:-1], bounds[1:]))
 
 
 def prefill_host(q, k, v, taus, out, head_dim=128, config=None):

@@ -196,3 +196,18 @@ def test_kv_group_sharding_two_ranks_gloo():
     full = sale.workload_gqa("sink_local", 7, 1, 256, 32, 8, 128, threads=2)
     want = [float(full[1][:, :, 4 * r:4 * r + 4].astype(np.int64).sum()) for r in range(2)]
     assert digests == want
+
+
+def test_query_block_split_balanced():
+    """a unit split across GPUs gets contiguous query-block
+    ranges with odd inner boundaries and about equal causal work (~ i^2)."""
+    for nq in (5, 64, 1000, 2048, 4096):
+        for parts in (1, 2, 3, 4, 8):
+            r = sale.query_block_split(nq, parts)
+            assert r[0][0] == 0 and r[-1][1] == nq
+            assert all(a < b for a, b in r) and all(r[k][1] == r[k + 1][0] for k in range(len(r) - 1))
+            assert all(b % 2 == 1 for _, b in r[:-1])
+            if nq >= 1000:
+                assert len(r) == parts
+                work = [(b * b - a * a) / (nq * nq) for a, b in r]
+                assert max(work) - min(work) < 0.02, (nq, parts, work)

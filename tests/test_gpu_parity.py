@@ -342,6 +342,30 @@ def test_chunked_host_pipeline_bit_identical(torch, B, N, Hq, Hkv):
     assert torch.equal(host_out.view(torch.int16), out.cpu().view(torch.int16))
 
 
+@pytest.mark.parametrize("B,N,Hq,Hkv,parts", [(1, 20000, 4, 1, 3), (2, 4100, 7, 1, 2)])
+def test_query_block_ranges_compose_to_the_full_prefill(torch, B, N, Hq, Hkv, parts):
+    """a (batch, KV group) unit split across GPUs by query-block
+    ranges (K/V replicated): the ranges' masks and outputs equal the one-shot
+    prefill bit for bit; the dense-mask attention likewise."""
+    inp = Inputs("sink_local", 17, B, N, Hq, Hkv)
+    q, k, v = inp.torch()
+    taus = [0.004 * (1 + h % 3) for h in range(Hq)]
+    nq, nk, nw = sale.grid(N)
+    full_mask = torch.zeros((B, Hq, nq, nw), dtype=torch.int32, device="cuda")
+    full = sale.prefill(q, k, v, taus, mask_out=full_mask)
+    dense = sale.block_sparse_attention(q, k, v, None)
+    mask = torch.zeros_like(full_mask)
+    for i0, i1 in sale.query_block_split(nq, parts):
+        part = sale.prefill(q, k, v, taus, mask_out=mask, q_blocks=(i0, i1))
+        t0, t1 = 64 * i0, min(64 * i1, N)
+        assert torch.equal(part[:, t0:t1].view(torch.int16), full[:, t0:t1].view(torch.int16))
+        dpart = sale.block_sparse_attention(q, k, v, None, q_blocks=(i0, i1))
+        assert torch.equal(dpart[:, t0:t1].view(torch.int16), dense[:, t0:t1].view(torch.int16))
+    assert torch.equal(mask, full_mask)
+    with pytest.raises(ValueError):
+        sale.prefill(q, k, v, taus, q_blocks=(2, nq))  # even inner boundary
+
+
 def test_invalid_arguments(torch):
     inp = Inputs("gaussian", 1, 1, 256, 4, 2)
     q, k, v = inp.torch()
