@@ -156,7 +156,13 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                     // epilogue of stage k-1 had three other heads' MMAs to finish.
                     // (The issue latency of this thread is on the critical path:
                     // the tensor pipe queues only a few MMAs, so nothing else here.)
-                    mbar_wait(&sm.tmem_empty[hh], (k & 1) ^ 1);
+                    if constexpr (prof) {
+                        const long long te = clock64();
+                        mbar_wait(&sm.tmem_empty[hh], (k & 1) ^ 1);
+                        w_empty += clock64() - te;
+                    } else {
+                        mbar_wait(&sm.tmem_empty[hh], (k & 1) ^ 1);
+                    }
                     tc_fence_after();
                     const uint32_t d = tmem + 128 * hh;
 #pragma unroll
