@@ -429,7 +429,7 @@ def run_b200(a):
             "estimation_overhead_pct": 100.0 * overhead, "density": density,
             "stage_ms": stage_ms, "effective_tflops": dense_flops / (ms_step * 1e-3) / 1e12,
             "tau_sweep": sweep, "roofline": roof, "clocks": clock,
-            "gpu_launches": 5 * a.steps}
+            "gpu_launches": (5 if split == 1 else 6) * a.steps}
     if "gather_ms" in main_r:
         line["output_gather_ms"] = main_r["gather_ms"]
     if second is not None:
