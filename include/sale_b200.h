@@ -34,6 +34,12 @@
  *
  * Streams: every call is stream-ordered and asynchronous unless it says
  * otherwise; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * A ctx owns workspace (codes, scales, thresholds, the default mask, taus,
+ * work-unit tables) shared by its calls: a call issued on a different stream
+ * than the previous workspace user first waits (cudaStreamWaitEvent) for that
+ * call's work, so calls on several streams are serialized on the device rather
+ * than racing. For concurrency, use one ctx per stream. Every entry point runs
+ * on the ctx's device and restores the caller's current device.
  */
 #ifndef SALE_B200_H
 #define SALE_B200_H
@@ -122,7 +128,13 @@ int sale_b200_select(sale_b200_ctx *ctx, const void *q, const void *k, const int
  * Replaces block_sparse_attention (sparse_attention.hpp:37); with
  * mask_words == NULL it is the all-true mask, i.e. full_attention
  * (attention.hpp:18). coverage (optional): int32 [B][Hq][N] attended tokens per
- * row (SparseAttentionOutput::coverage). */
+ * row (SparseAttentionOutput::coverage).
+ * A row that attends no token returns SALE_B200_DOMAIN_ERROR naming the first
+ * such row, as the reference throws std::domain_error (sparse_attention.hpp:
+ * 88-90): with a caller mask the call therefore waits for the kernel
+ * (synchronous, like the reference). mask_words == NULL is asynchronous. The
+ * prefill entry points never check: the Selection-Pass always keeps the sink
+ * block, which every row attends. */
 int sale_b200_sparse_attention(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
                                const sale_b200_shape *shape, const uint32_t *mask_words,
                                void *out, int32_t *coverage, void *stream);

@@ -67,6 +67,8 @@ def _load_c():
     lib.oracle_selection_pass.argtypes = [f32p, f32p, i64, i64, i8p, f32p, i8p, f32p,
                                           C.POINTER(Cfg), u8p, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p]
+    lib.oracle_selection_stats.argtypes = [f32p, f32p, i64, i64, C.POINTER(Cfg), i64, i64, f64p,
+                                           f64p, f64p]
     lib.oracle_block_sparse_attention.argtypes = [f32p, f32p, f32p, i64, i64, u8p, i64, i64,
                                                   f32p, i64p]
     lib.oracle_full_attention.argtypes = [f32p, f32p, f32p, i64, i64, f32p]
@@ -96,6 +98,8 @@ def _load_ref():
     lib.ref_workload_head.argtypes = [C.c_int, C.c_uint64, i64, i64, i64, f32p, f32p, f32p]
     lib.ref_run_pipeline.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, i64, f64p,
                                      f64p, f64p]
+    lib.ref_workload_gqa_heads.argtypes = [C.c_int, C.c_uint64, i64, i64, i64, i64, C.c_int, i64,
+                                           f32p, f32p, f32p]
     lib.ref_sale_heads.argtypes = [f32p, f32p, f32p, i64, i64, i64, C.c_double, i64, f64p, f64p]
     lib.ref_run_report.argtypes = [f32p, f32p, f32p, i64, i64, i64, f64p, C.c_int, i64, f64p]
     lib.ref_sweep.argtypes = [f32p, f32p, f32p, i64, i64, i64, f64p, i64, i64, f64p]
@@ -161,6 +165,19 @@ def selection_pass(q, k, qcodes, qscales, kcodes, kscales, c=None, debug=False):
     if st:
         raise ValueError(f"selection_pass: status {st}")
     return (mask, dbg) if debug else mask
+
+
+def selection_stats(q, k, c=None, i_lo=0, i_hi=-1):
+    """The statistics of selection_pass (selection.hpp:224-251): (m, l, bound)
+    float64 [tokens], NaN for rows whose query block has an empty middle."""
+    c = c or cfg()
+    q, k = _f32(q), _f32(k)
+    n, d = q.shape
+    m, l, b = (np.full(n, np.nan) for _ in range(3))
+    st = C_LIB.oracle_selection_stats(q, k, n, d, C.byref(c), i_lo, i_hi, m, l, b)
+    if st:
+        raise ValueError(f"selection_stats: status {st}")
+    return m, l, b
 
 
 def block_sparse_attention(q, k, v, mask, block_q=64, block_k=32):

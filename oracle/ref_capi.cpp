@@ -17,7 +17,9 @@
 #include <sale/sparse_attention.hpp>
 #include <sale/workloads.hpp>
 
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -217,6 +219,85 @@ int ref_workload_head(int kind, uint64_t seed, int64_t n, int64_t d, int64_t hea
         std::memcpy(q, h.query.data().data(), bytes);
         std::memcpy(k, h.key.data().data(), bytes);
         std::memcpy(v, h.value.data().data(), bytes);
+    });
+}
+
+// The GQA extension of sink_local_head / gaussian_head (the
+// product's generator is paper_2505_24179_b200/csrc/workload.cpp, pinned to
+// this one by tests/test_abi.py) built from the reference's own Rng,
+// head_rng, fill_normal, random_unit and generators (workloads.hpp:17-159):
+// KV group g = reference head g (its K, V and, for r = 0, its Q); query head
+// r > 0 of the group = fresh N(0,1) noise from the reference Rng seeded
+// seed + kQStream * r (head_rng of head g) plus the same planted terms. Output
+// per Q head h (K / V of its group replicated): [q_heads][n][d] fp32, rounded
+// to bf16 (RNE) when round_bf16 — the values the B200 path receives. Batch 0.
+// Lets bench.py's reference arm build its inputs without the product library.
+int ref_workload_gqa_heads(int kind, uint64_t seed, int64_t n, int64_t d, int64_t q_heads,
+                           int64_t kv_heads, int round_bf16, int64_t threads, float *q, float *k,
+                           float *v) {
+    constexpr std::uint64_t kQStream = 0xD1B54A32D192ED03ULL;
+    return guarded([&] {
+        if (q_heads % kv_heads) throw std::invalid_argument("q_heads % kv_heads");
+        const int64_t G = q_heads / kv_heads;
+        const std::size_t nd = static_cast<std::size_t>(n * d);
+        auto bf16 = [&](float x) {
+            if (!round_bf16) return x;
+            std::uint32_t u;
+            std::memcpy(&u, &x, 4);
+            u += 0x7FFFu + ((u >> 16) & 1u);
+            u &= 0xFFFF0000u;
+            float y;
+            std::memcpy(&y, &u, 4);
+            return y;
+        };
+        parallel_for(static_cast<std::size_t>(q_heads), static_cast<std::size_t>(threads),
+                     [&](std::size_t h) {
+            const std::size_t g = h / G, r = h % G;
+            WorkloadSpec spec;
+            spec.seed = seed;
+            spec.tokens = static_cast<std::size_t>(n);
+            spec.head_dim = static_cast<std::size_t>(d);
+            spec.heads = g + 1;
+            spec.kind = kind == 0 ? WorkloadKind::Gaussian : WorkloadKind::SinkLocal;
+            const HeadInput base = kind == 0 ? detail::gaussian_head(spec, g)
+                                             : detail::sink_local_head(spec, g);
+            DenseMatrix qr = base.query;
+            if (r > 0) {
+                WorkloadSpec s2 = spec;
+                s2.seed = seed + kQStream * r;
+                Rng noise = detail::head_rng(s2, g);
+                detail::fill_normal(noise, qr);
+                if (kind == 1) { // the planted query terms of head g (workloads.hpp:128-158)
+                    Rng rng = detail::head_rng(spec, g);
+                    for (std::size_t t = 0; t < 3 * nd; ++t) (void)rng.next_normal();
+                    const double sqrt_d = std::sqrt(static_cast<double>(d));
+                    const double sink_amp = std::sqrt(std::max(spec.sink_logit, 0.0) * sqrt_d);
+                    const double local_amp = std::sqrt(std::max(spec.local_logit, 0.0) * sqrt_d);
+                    const double rho = std::exp(-1.0 / spec.local_decay_tokens);
+                    const double drift = std::sqrt(1.0 - rho * rho);
+                    const std::vector<double> sink_dir = detail::random_unit(rng, d);
+                    std::vector<double> local_dir = detail::random_unit(rng, d);
+                    for (int64_t i = 0; i < n; ++i) {
+                        if (i > 0) {
+                            double norm2 = 0.0;
+                            for (int64_t c = 0; c < d; ++c) {
+                                local_dir[c] = rho * local_dir[c] + drift * rng.next_normal() / sqrt_d;
+                                norm2 += local_dir[c] * local_dir[c];
+                            }
+                            const double inv = 1.0 / std::sqrt(norm2 > 0.0 ? norm2 : 1.0);
+                            for (auto &x : local_dir) x *= inv;
+                        }
+                        for (int64_t c = 0; c < d; ++c)
+                            qr(i, c) += static_cast<float>(sink_amp * sink_dir[c] + local_amp * local_dir[c]);
+                    }
+                }
+            }
+            for (std::size_t e = 0; e < nd; ++e) {
+                q[h * nd + e] = bf16(qr.data()[e]);
+                k[h * nd + e] = bf16(base.key.data()[e]);
+                v[h * nd + e] = bf16(base.value.data()[e]);
+            }
+        });
     });
 }
 

@@ -318,6 +318,46 @@ int oracle_selection_pass(const float *q, const float *k, int64_t tokens, int64_
     return OK;
 }
 
+/* The statistics part of oracle_selection_pass alone (selection.hpp:224-251):
+ * m, l and bound [tokens] for every query block with a non-empty middle
+ * region (NaN elsewhere). Same loop, same calls; for parity runs at sizes
+ * where the middle-block estimates are restated with exact BLAS products. */
+int oracle_selection_stats(const float *q, const float *k, int64_t tokens, int64_t d,
+                           const oracle_cfg *cfg, int64_t i_lo, int64_t i_hi, double *m_out,
+                           double *l_out, double *bound_out) {
+    if (oracle_config_validate(cfg)) return E_INVALID;
+    if (tokens == 0 || d == 0) return E_INVALID;
+    const grid_t g = make_grid(tokens, cfg->block_q, cfg->block_k);
+    const int64_t sink_blocks = (imin(cfg->sink_tokens, tokens) + g.bk - 1) / g.bk;
+    int64_t *sl = (int64_t *)malloc(sizeof(int64_t) * (size_t)g.nk);
+    double *m = (double *)malloc(sizeof(double) * (size_t)g.bq);
+    double *l = (double *)malloc(sizeof(double) * (size_t)g.bq);
+    if (i_hi > g.nq || i_hi < 0) i_hi = g.nq;
+    for (int64_t i = i_lo; i < i_hi; ++i) {
+        const int64_t q0 = qbeg(&g, i), q1 = qend(&g, i);
+        for (int64_t r = q0; r < q1; ++r) m_out[r] = l_out[r] = bound_out[r] = NAN;
+        const int64_t nsl = oracle_sink_local_index_set(i, tokens, cfg, sl);
+        const int64_t mb = imin(sink_blocks, g.nk);
+        int64_t me = mb;
+        for (int64_t s = 0; s < nsl; ++s)
+            if (sl[s] >= sink_blocks) {
+                me = imax(mb, sl[s]);
+                break;
+            }
+        if (me == mb) continue;
+        oracle_sink_local_stats(q, k, tokens, d, g.bq, g.bk, i, sl, nsl, m, l);
+        for (int64_t r = 0; r < q1 - q0; ++r) {
+            m_out[q0 + r] = m[r];
+            l_out[q0 + r] = l[r];
+            bound_out[q0 + r] = oracle_threshold_bound(cfg->tau, m[r], l[r]);
+        }
+    }
+    free(sl);
+    free(m);
+    free(l);
+    return OK;
+}
+
 /* ------------------------------------------------------ sparse_attention.hpp */
 
 /* sparse_attention.hpp:37-97 — exact attention over the selected blocks,

@@ -41,6 +41,7 @@
 //           TMEM only when the running max grows by > 8); P -> bf16 ->
 //           tcgen05.st over S.
 #include "common.cuh"
+#include "internal.h"
 
 namespace sale_b200 {
 
@@ -282,8 +283,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const uint32_t *__restrict__ mask,
                         __nv_bfloat16 *__restrict__ out, int32_t *__restrict__ coverage,
-                        int64_t tokens, int hq, int hkv, float scale_log2, int64_t i_lo,
-                        int64_t ni) {
+                        unsigned long long *__restrict__ empty_rows, int64_t tokens, int hq, int hkv,
+                        float scale_log2, int64_t i_lo, int64_t ni) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const long long t_kernel = clock64();
     AttnSmem &sm = *reinterpret_cast<AttnSmem *>(smem_raw + smem_pad_1k(smem_raw));
@@ -658,6 +659,14 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             if (ok0) cv[grow0] = ct[0];
             if (ok1) cv[grow1] = ct[1];
         }
+        // a row that attends no token: block_sparse_attention throws
+        // std::domain_error for the first such row (sparse_attention.hpp:88-90);
+        // the ABI reports the smallest (b, h, row) index
+        if (q4 == 0 && empty_rows) {
+            const unsigned long long base = (static_cast<unsigned long long>(b) * hq + h) * tokens;
+            if (ok1 && ct[1] == 0) atomicMin(empty_rows, base + grow1);
+            if (ok0 && ct[0] == 0) atomicMin(empty_rows, base + grow0);
+        }
         if (prof) atomicAdd(&g_attn_prof[10], static_cast<unsigned long long>(clock64() - t_epi));
     }
     tc_fence_before();
@@ -687,27 +696,21 @@ size_t attention_smem_bytes() { return sizeof(AttnSmem) + 1024; }
 cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
                                     const uint32_t *mask, void *out, int32_t *coverage,
                                     int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
-                                    cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
+                                    cudaStream_t stream, int64_t i_lo, int64_t i_hi,
+                                    unsigned long long *empty_rows) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     if (nq / 2 + 3 > kMaxTiles) return cudaErrorInvalidValue;
-    static bool configured = false;
     const size_t smem = attention_smem_bytes();
-    if (!configured) {
-        for (auto kern : {sparse_attention_kernel<false>, sparse_attention_kernel<true>}) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-        }
-        configured = true;
-    }
     const int npairs = (hq / hkv + 1) / 2;
     if (i_hi < 0 || i_hi > nq) i_hi = nq;
     if (i_hi <= i_lo) return cudaSuccess;
     const int64_t grid = batch * hkv * npairs * (i_hi - i_lo);
     auto kern = g_attn_prof_host ? sparse_attention_kernel<true> : sparse_attention_kernel<false>;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
+    if (e != cudaSuccess) return e;
     kern<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
         static_cast<const __nv_bfloat16 *>(q), tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out),
-        coverage, tokens, hq, hkv, scale_log2, i_lo, i_hi - i_lo);
+        coverage, empty_rows, tokens, hq, hkv, scale_log2, i_lo, i_hi - i_lo);
     return cudaGetLastError();
 }
 

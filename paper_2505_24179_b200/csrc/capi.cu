@@ -47,6 +47,14 @@ struct sale_b200_ctx {
     // optional per-stage event timing of sale_b200_prefill
     bool timing = false;
     cudaEvent_t ev[6] = {};
+    // stream ordering of the ctx-owned workspace: the last call that used it
+    // recorded ws_ev on ws_stream; a call on another stream waits for it
+    cudaEvent_t ws_ev = nullptr;
+    cudaStream_t ws_stream = nullptr;
+    // empty-row check of block_sparse_attention with a caller mask: smallest
+    // (b, h, row) index that attends nothing (device) and its pinned copy
+    unsigned long long *d_empty = nullptr;
+    unsigned long long *h_empty = nullptr;
 };
 
 namespace {
@@ -70,6 +78,64 @@ int cuda_fail(sale_b200_ctx *ctx, cudaError_t e, const char *where) {
     } while (0)
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Every ctx entry point runs on ctx's device and restores the caller's
+// current device on return (a process may drive one ctx per GPU).
+struct DeviceGuard {
+    int prev = -1, dev;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int d) : dev(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+#define SALE_ENTER(ctx)                                                                            \
+    if (!(ctx)) return SALE_B200_INVALID_ARGUMENT;                                                 \
+    std::lock_guard<std::mutex> lk_((ctx)->mu);                                                    \
+    DeviceGuard dg_((ctx)->device);                                                                \
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice")
+
+// Workspace hand-off between streams (see the ctx fields).
+int ws_begin(sale_b200_ctx *ctx, cudaStream_t stream) {
+    if (ctx->ws_ev && ctx->ws_stream != stream)
+        SALE_CUDA(ctx, cudaStreamWaitEvent(stream, ctx->ws_ev, 0));
+    return SALE_B200_OK;
+}
+int ws_end(sale_b200_ctx *ctx, cudaStream_t stream) {
+    if (!ctx->ws_ev) SALE_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ws_ev, cudaEventDisableTiming));
+    SALE_CUDA(ctx, cudaEventRecord(ctx->ws_ev, stream));
+    ctx->ws_stream = stream;
+    return SALE_B200_OK;
+}
+
+// block_sparse_attention's domain_error (sparse_attention.hpp:88-90) for a
+// caller-supplied mask: the kernel records the smallest empty (b, h, row)
+// index; the call waits for it (the reference is synchronous) and reports it.
+int empty_rows_begin(sale_b200_ctx *ctx, cudaStream_t stream) {
+    if (!ctx->d_empty) {
+        SALE_CUDA(ctx, cudaMalloc(&ctx->d_empty, sizeof(unsigned long long)));
+        SALE_CUDA(ctx, cudaMallocHost(&ctx->h_empty, sizeof(unsigned long long)));
+    }
+    SALE_CUDA(ctx, cudaMemsetAsync(ctx->d_empty, 0xFF, sizeof(unsigned long long), stream));
+    return SALE_B200_OK;
+}
+int empty_rows_end(sale_b200_ctx *ctx, cudaStream_t stream, int64_t batch, int64_t q_heads,
+                   int64_t tokens) {
+    SALE_CUDA(ctx, cudaMemcpyAsync(ctx->h_empty, ctx->d_empty, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, stream));
+    SALE_CUDA(ctx, cudaStreamSynchronize(stream));
+    const unsigned long long x = *ctx->h_empty;
+    if (x == ~0ull) return SALE_B200_OK;
+    const int64_t row = static_cast<int64_t>(x % static_cast<unsigned long long>(tokens));
+    const int64_t bh = static_cast<int64_t>(x / static_cast<unsigned long long>(tokens));
+    std::string msg = "block_sparse_attention: query row " + std::to_string(row) + " attends no tokens";
+    if (batch * q_heads > 1)
+        msg += " (batch " + std::to_string(bh / q_heads) + ", head " + std::to_string(bh % q_heads) + ")";
+    return fail(ctx, SALE_B200_DOMAIN_ERROR, msg);
+}
 
 // Stage boundaries: 0 start, 1 quantized, 2 base mask, 3 stats, 4 estimate, 5 attention.
 void mark(sale_b200_ctx *ctx, int i, cudaStream_t stream) {
@@ -141,13 +207,17 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // 4-D map over [B][N][H][128] with a SWIZZLE_128B box of
 // {box_inner elements, 1 head, box_rows tokens, 1 batch}.
+// rows_limit (> 0): the map covers tokens [0, rows_limit) of each batch (the
+// batch stride stays tokens rows); TMA zero-fills rows past it.
 int make_map(sale_b200_ctx *ctx, CUtensorMap *map, const void *base, bool bf16, int64_t batch,
-             int64_t tokens, int64_t heads, uint32_t box_inner, uint32_t box_rows) {
+             int64_t tokens, int64_t heads, uint32_t box_inner, uint32_t box_rows,
+             int64_t rows_limit = 0) {
     auto enc = tensor_map_encoder();
     if (!enc) return fail(ctx, SALE_B200_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
     const uint64_t eb = bf16 ? 2 : 1;
     cuuint64_t dims[4] = {static_cast<cuuint64_t>(kHeadDim), static_cast<cuuint64_t>(heads),
-                          static_cast<cuuint64_t>(tokens), static_cast<cuuint64_t>(batch)};
+                          static_cast<cuuint64_t>(rows_limit > 0 ? rows_limit : tokens),
+                          static_cast<cuuint64_t>(batch)};
     cuuint64_t strides[3] = {kHeadDim * eb, static_cast<cuuint64_t>(heads) * kHeadDim * eb,
                              static_cast<cuuint64_t>(tokens * heads) * kHeadDim * eb};
     cuuint32_t box[4] = {box_inner, 1, box_rows, 1};
@@ -282,7 +352,8 @@ int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *
 
 int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
                    const sale_b200_shape &s, const uint32_t *mask, void *out, int32_t *coverage,
-                   cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1) {
+                   cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1,
+                   unsigned long long *empty_rows = nullptr) {
     int st;
     CUtensorMap tk, tv;
     if ((st = make_map(ctx, &tk, k, true, s.batch, s.tokens, s.kv_heads, 64, 128))) return st;
@@ -290,7 +361,7 @@ int attention_impl(sale_b200_ctx *ctx, const void *q, const void *k, const void 
     const float scale_log2 = inv_sqrt_dim(s.head_dim) * 1.4426950408889634f;
     SALE_CUDA(ctx, launch_sparse_attention(q, tk, tv, mask, out, coverage, s.batch, s.tokens,
                                            static_cast<int>(s.q_heads), static_cast<int>(s.kv_heads),
-                                           scale_log2, stream, i_lo, i_hi));
+                                           scale_log2, stream, i_lo, i_hi, empty_rows));
     mark(ctx, 5, stream);
     return SALE_B200_OK;
 }
@@ -376,6 +447,19 @@ int ensure_chunk_units(sale_b200_ctx *ctx, int64_t tokens, const std::vector<int
 
 namespace sale_b200 {
 int set_error(sale_b200_ctx *ctx, int code, const std::string &msg) { return fail(ctx, code, msg); }
+cudaError_t ensure_smem_attr(const void *func, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, const void *>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto &x : done)
+        if (x.first == dev && x.second == func) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e == cudaSuccess) done.emplace_back(dev, func);
+    return e;
+}
 int ctx_device_of(const sale_b200_ctx *ctx) { return ctx->device; }
 } // namespace sale_b200
 
@@ -417,43 +501,56 @@ int sale_b200_ctx_create(int device, sale_b200_ctx **out) {
 
 int sale_b200_device_alloc(sale_b200_ctx *ctx, uint64_t bytes, void **out) {
     if (!ctx || !out) return SALE_B200_INVALID_ARGUMENT;
-    SALE_CUDA(ctx, cudaSetDevice(ctx->device));
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     SALE_CUDA(ctx, cudaMalloc(out, bytes ? bytes : 1));
     return SALE_B200_OK;
 }
 
 int sale_b200_device_free(sale_b200_ctx *ctx, void *ptr) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     if (ptr) SALE_CUDA(ctx, cudaFree(ptr));
     return SALE_B200_OK;
 }
 
 int sale_b200_copy_to_device(sale_b200_ctx *ctx, void *dst, const void *src, uint64_t bytes) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     SALE_CUDA(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
     return SALE_B200_OK;
 }
 
 int sale_b200_copy_to_host(sale_b200_ctx *ctx, void *dst, const void *src, uint64_t bytes) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     SALE_CUDA(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
     return SALE_B200_OK;
 }
 
 int sale_b200_memset(sale_b200_ctx *ctx, void *dst, int value, uint64_t bytes) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     SALE_CUDA(ctx, cudaMemset(dst, value, bytes));
     return SALE_B200_OK;
 }
 
 int sale_b200_synchronize(sale_b200_ctx *ctx) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     SALE_CUDA(ctx, cudaDeviceSynchronize());
     return SALE_B200_OK;
 }
 
 int sale_b200_estimator_profile(sale_b200_ctx *ctx, int enable, uint64_t *counters) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     SALE_CUDA(ctx, cudaDeviceSynchronize());
     SALE_CUDA(ctx, estimate_profile(enable, reinterpret_cast<unsigned long long *>(counters)));
     SALE_CUDA(ctx, stats_profile(enable, counters ? reinterpret_cast<unsigned long long *>(counters + 8)
@@ -463,14 +560,15 @@ int sale_b200_estimator_profile(sale_b200_ctx *ctx, int enable, uint64_t *counte
 
 int sale_b200_attention_profile(sale_b200_ctx *ctx, int enable, uint64_t *counters) {
     if (!ctx) return SALE_B200_INVALID_ARGUMENT;
+    DeviceGuard dg_(ctx->device);
+    if (dg_.err != cudaSuccess) return cuda_fail(ctx, dg_.err, "cudaSetDevice");
     SALE_CUDA(ctx, cudaDeviceSynchronize());
     SALE_CUDA(ctx, attention_profile(enable, reinterpret_cast<unsigned long long *>(counters)));
     return SALE_B200_OK;
 }
 
 int sale_b200_set_timing(sale_b200_ctx *ctx, int enable) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     if (enable && !ctx->ev[0])
         for (auto &e : ctx->ev) SALE_CUDA(ctx, cudaEventCreate(&e));
     ctx->timing = enable != 0;
@@ -478,8 +576,8 @@ int sale_b200_set_timing(sale_b200_ctx *ctx, int enable) {
 }
 
 int sale_b200_stage_times(sale_b200_ctx *ctx, float *ms) {
-    if (!ctx || !ms) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ms) return SALE_B200_INVALID_ARGUMENT;
+    SALE_ENTER(ctx);
     if (!ctx->ev[0]) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "timing was never enabled");
     SALE_CUDA(ctx, cudaEventSynchronize(ctx->ev[5]));
     for (int i = 0; i < 5; ++i) SALE_CUDA(ctx, cudaEventElapsedTime(&ms[i], ctx->ev[i], ctx->ev[i + 1]));
@@ -499,6 +597,9 @@ void sale_b200_ctx_destroy(sale_b200_ctx *ctx) {
     if (ctx->comp_stream) cudaStreamDestroy(ctx->comp_stream);
     if (ctx->out_stream) cudaStreamDestroy(ctx->out_stream);
     if (ctx->d_cunits) cudaFree(ctx->d_cunits);
+    if (ctx->ws_ev) cudaEventDestroy(ctx->ws_ev);
+    if (ctx->d_empty) cudaFree(ctx->d_empty);
+    if (ctx->h_empty) cudaFreeHost(ctx->h_empty);
     delete ctx;
 }
 
@@ -509,8 +610,7 @@ const char *sale_b200_last_error(const sale_b200_ctx *ctx) {
 int sale_b200_quantize(sale_b200_ctx *ctx, const void *x, int64_t batch, int64_t tokens,
                        int64_t heads, int64_t group_rows, int8_t *codes, float *scales,
                        void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     if (!x || !codes || !scales) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
     if (batch < 1 || tokens < 1 || heads < 1)
         return fail(ctx, SALE_B200_INVALID_ARGUMENT, "quantize: empty input");
@@ -532,8 +632,7 @@ int sale_b200_quantize(sale_b200_ctx *ctx, const void *x, int64_t batch, int64_t
 int sale_b200_quantize_qk(sale_b200_ctx *ctx, const void *q, const void *k,
                           const sale_b200_shape *shape, int8_t *q_codes, float *q_scales,
                           int8_t *k_codes, float *k_scales, void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     int st;
     if ((st = check_shape(ctx, shape))) return st;
     if (!q || !k || !q_codes || !q_scales || !k_codes || !k_scales)
@@ -549,8 +648,7 @@ int sale_b200_select(sale_b200_ctx *ctx, const void *q, const void *k, const int
                      const sale_b200_shape *shape, const double *taus,
                      const sale_b200_selection_config *cfg, uint32_t *mask_words,
                      const sale_b200_select_debug *dbg, void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     int st;
     if ((st = check_shape(ctx, shape))) return st;
     if ((st = check_config(ctx, cfg))) return st;
@@ -559,26 +657,34 @@ int sale_b200_select(sale_b200_ctx *ctx, const void *q, const void *k, const int
         return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
     Workspace w;
     if ((st = ensure_workspace(ctx, *shape, &w))) return st;
-    return select_impl(ctx, q, k, q_codes, q_scales, k_codes, k_scales, *shape, taus, mask_words,
-                       w.thresh, dbg, static_cast<cudaStream_t>(stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if ((st = ws_begin(ctx, s))) return st;
+    if ((st = select_impl(ctx, q, k, q_codes, q_scales, k_codes, k_scales, *shape, taus, mask_words,
+                          w.thresh, dbg, s)))
+        return st;
+    return ws_end(ctx, s);
 }
 
 int sale_b200_sparse_attention(sale_b200_ctx *ctx, const void *q, const void *k, const void *v,
                                const sale_b200_shape *shape, const uint32_t *mask_words,
                                void *out, int32_t *coverage, void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     int st;
     if ((st = check_shape(ctx, shape))) return st;
     if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
-    return attention_impl(ctx, q, k, v, *shape, mask_words, out, coverage,
-                          static_cast<cudaStream_t>(stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!mask_words) // all-true mask: every row attends its causal prefix
+        return attention_impl(ctx, q, k, v, *shape, nullptr, out, coverage, s);
+    if ((st = ws_begin(ctx, s)) || (st = empty_rows_begin(ctx, s))) return st;
+    if ((st = attention_impl(ctx, q, k, v, *shape, mask_words, out, coverage, s, 0, -1, ctx->d_empty)))
+        return st;
+    if ((st = ws_end(ctx, s))) return st;
+    return empty_rows_end(ctx, s, shape->batch, shape->q_heads, shape->tokens);
 }
 
 int sale_b200_flop_count(sale_b200_ctx *ctx, const uint32_t *mask_words, int64_t batch,
                          int64_t q_heads, int64_t tokens, int64_t *counts, void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     if (!mask_words || !counts) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
     if (batch < 1 || q_heads < 1 || tokens < 1)
         return fail(ctx, SALE_B200_INVALID_ARGUMENT, "flop_accounting: empty grid");
@@ -591,8 +697,7 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
                       const sale_b200_shape *shape, const double *taus,
                       const sale_b200_selection_config *cfg, void *out, uint32_t *mask_out,
                       void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     int st;
     if ((st = check_shape(ctx, shape))) return st;
     if ((st = check_config(ctx, cfg))) return st;
@@ -602,6 +707,7 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
     if ((st = ensure_workspace(ctx, *shape, &w))) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uint32_t *mask = mask_out ? mask_out : w.mask;
+    if ((st = ws_begin(ctx, s))) return st;
     mark(ctx, 0, s);
     SALE_CUDA(ctx, launch_quantize_qk(q, k, w.q_codes, w.q_scales, w.k_codes, w.k_scales,
                                       shape->batch, shape->tokens, shape->q_heads,
@@ -610,7 +716,10 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
     if ((st = select_impl(ctx, q, k, w.q_codes, w.q_scales, w.k_codes, w.k_scales, *shape, taus,
                           mask, w.thresh, nullptr, s)))
         return st;
-    return attention_impl(ctx, q, k, v, *shape, mask, out, nullptr, s);
+    // The Selection-Pass always keeps the sink block (selection.hpp:228-232),
+    // which every row attends (token 0), so no row can be empty here.
+    if ((st = attention_impl(ctx, q, k, v, *shape, mask, out, nullptr, s))) return st;
+    return ws_end(ctx, s);
 }
 
 // A query-block range [i_lo, i_hi) of the prefill (one GPU's share when a
@@ -632,8 +741,7 @@ int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, co
                             const sale_b200_shape *shape, const double *taus,
                             const sale_b200_selection_config *cfg, int64_t i_lo, int64_t i_hi,
                             void *out, uint32_t *mask_out, void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     int st;
     if ((st = check_shape(ctx, shape))) return st;
     if ((st = check_config(ctx, cfg))) return st;
@@ -652,6 +760,7 @@ int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, co
     if (i_hi < nq) bounds.push_back(i_hi);
     bounds.push_back(nq);
     const size_t grp = i_lo > 0 ? 1 : 0; // the unit group of [i_lo, i_hi)
+    if ((st = ws_begin(ctx, s))) return st;
     if ((st = upload_taus(ctx, taus, Hq, s))) return st;
     if ((st = ensure_chunk_units(ctx, N, bounds, s))) return st;
     const int64_t t0 = i_lo * kBlockQ, t1 = std::min<int64_t>(i_hi * kBlockQ, N);
@@ -677,28 +786,33 @@ int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, co
                                        static_cast<int>(Hkv), isd, nullptr, s));
     }
     mark(ctx, 4, s);
-    return attention_impl(ctx, q, k, v, sh, mask, out, nullptr, s, i_lo, i_hi);
+    if ((st = attention_impl(ctx, q, k, v, sh, mask, out, nullptr, s, i_lo, i_hi))) return st;
+    return ws_end(ctx, s);
 }
 
 int sale_b200_sparse_attention_range(sale_b200_ctx *ctx, const void *q, const void *k,
                                      const void *v, const sale_b200_shape *shape,
                                      const uint32_t *mask_words, int64_t i_lo, int64_t i_hi,
                                      void *out, int32_t *coverage, void *stream) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     int st;
     if ((st = check_shape(ctx, shape))) return st;
     if ((st = check_range(ctx, shape, i_lo, i_hi))) return st;
     if (!q || !k || !v || !out) return fail(ctx, SALE_B200_INVALID_ARGUMENT, "NULL buffer");
-    return attention_impl(ctx, q, k, v, *shape, mask_words, out, coverage,
-                          static_cast<cudaStream_t>(stream), i_lo, i_hi);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!mask_words) return attention_impl(ctx, q, k, v, *shape, nullptr, out, coverage, s, i_lo, i_hi);
+    if ((st = ws_begin(ctx, s)) || (st = empty_rows_begin(ctx, s))) return st;
+    if ((st = attention_impl(ctx, q, k, v, *shape, mask_words, out, coverage, s, i_lo, i_hi,
+                             ctx->d_empty)))
+        return st;
+    if ((st = ws_end(ctx, s))) return st;
+    return empty_rows_end(ctx, s, shape->batch, shape->q_heads, shape->tokens);
 }
 
 int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t *k,
                            const uint16_t *v, const sale_b200_shape *shape, const double *taus,
                            const sale_b200_selection_config *cfg, uint16_t *out) {
-    if (!ctx) return SALE_B200_INVALID_ARGUMENT;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    SALE_ENTER(ctx);
     int st;
     if ((st = check_shape(ctx, shape))) return st;
     if ((st = check_config(ctx, cfg))) return st;
@@ -714,6 +828,7 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
         ctx->io_bytes = 0;
         SALE_CUDA(ctx, cudaMalloc(&ctx->io, need));
         ctx->io_bytes = need;
+        SALE_CUDA(ctx, cudaMemset(ctx->io, 0, need));
     }
     for (cudaStream_t *p : {&ctx->io_stream, &ctx->comp_stream, &ctx->out_stream})
         if (!*p) SALE_CUDA(ctx, cudaStreamCreateWithFlags(p, cudaStreamNonBlocking));
@@ -721,22 +836,25 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
             *dout = dv + align256(kbytes);
     cudaStream_t s_in = ctx->io_stream, s_comp = ctx->comp_stream, s_out = ctx->out_stream;
     // The prefill in token chunks, three streams: the H2D copy of chunk c+1 and
-    // the D2H copy of chunk c-1 run under chunk c's kernels. Every stage only
-    // reads data of its own and earlier chunks (causal), so the result is
-    // bit-identical to the one-shot sale_b200_prefill.
+    // the D2H copy of chunk c-1 run under chunk c's kernels. Every stage reads
+    // only data of its own and earlier chunks (causal): the attention's last
+    // 128-key K / V tile may extend past the chunk end t1 (into rows the H2D of
+    // chunk c+1 is still writing), so chunk c's K / V tensor maps end at t1 and
+    // TMA fills those rows with zeros (their P is 0; stale data there could be
+    // NaN, and 0 * NaN would poison the row). The result is bit-identical to the
+    // one-shot sale_b200_prefill.
     const int64_t nq = cdiv(N, kBlockQ);
     const std::vector<int64_t> bounds =
         N >= 65536 ? chunk_bounds_long(nq) : chunk_bounds(nq, N >= 16384 ? 8 : (N >= 2048 ? 4 : 1));
     const size_t nch = bounds.size() - 1;
     Workspace w;
     if ((st = ensure_workspace(ctx, s, &w))) return st;
+    if ((st = ws_begin(ctx, s_comp))) return st;
     if ((st = upload_taus(ctx, taus, Hq, s_comp))) return st;
     if ((st = ensure_chunk_units(ctx, N, bounds, s_comp))) return st;
-    CUtensorMap tm_qc, tm_kc, tk, tv;
+    CUtensorMap tm_qc, tm_kc;
     if ((st = make_map(ctx, &tm_qc, w.q_codes, false, B, N, Hq, 128, 128))) return st;
     if ((st = make_map(ctx, &tm_kc, w.k_codes, false, B, N, Hkv, 128, 128))) return st;
-    if ((st = make_map(ctx, &tk, dk, true, B, N, Hkv, 64, 128))) return st;
-    if ((st = make_map(ctx, &tv, dv, true, B, N, Hkv, 64, 128))) return st;
     const float isd = inv_sqrt_dim(s.head_dim);
     const float scale_log2 = isd * 1.4426950408889634f;
     std::vector<cudaEvent_t> ev(2 * nch);
@@ -773,6 +891,9 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
             SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_cunits + u0, u1 - u0, w.q_scales,
                                            w.k_scales, w.thresh, w.mask, B, N, static_cast<int>(Hq),
                                            static_cast<int>(Hkv), isd, nullptr, s_comp));
+        CUtensorMap tk, tv; // K / V rows [0, t1) of the [B][N][Hkv][128] layout
+        if ((st = make_map(ctx, &tk, dk, true, B, N, Hkv, 64, 128, t1))) return st;
+        if ((st = make_map(ctx, &tv, dv, true, B, N, Hkv, 64, 128, t1))) return st;
         SALE_CUDA(ctx, launch_sparse_attention(dq, tk, tv, w.mask, dout, nullptr, B, N,
                                                static_cast<int>(Hq), static_cast<int>(Hkv),
                                                scale_log2, s_comp, i0, i1));
@@ -782,7 +903,7 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
     }
     SALE_CUDA(ctx, cudaStreamSynchronize(s_out));
     SALE_CUDA(ctx, cudaStreamSynchronize(s_comp));
-    return SALE_B200_OK;
+    return ws_end(ctx, s_comp);
 }
 
 } // extern "C"

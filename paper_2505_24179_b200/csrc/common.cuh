@@ -13,6 +13,13 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// A wait on an mbarrier longer than this traps (turns a protocol bug into a
+// launch error instead of a hung GPU). The compute-sanitizer build raises it:
+// instrumented kernels run orders of magnitude slower.
+#ifndef SALE_B200_WAIT_TIMEOUT_NS
+#define SALE_B200_WAIT_TIMEOUT_NS 4000000000ull
+#endif
+
 namespace sale_b200 {
 
 constexpr int kHeadDim = 128;   // storage pitch of every row (elements)
@@ -95,7 +102,7 @@ __device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
     while (!mbar_test_wait(a, parity)) {
         if ((++spins & 4095u) == 0) {
             if (t0 == 0) t0 = global_timer_ns();
-            else if (global_timer_ns() - t0 > 4000000000ull) __trap();
+            else if (global_timer_ns() - t0 > SALE_B200_WAIT_TIMEOUT_NS) __trap();
         }
     }
 }
@@ -108,7 +115,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint64_t t0 = global_timer_ns();
     uint32_t spins = 0;
     while (!mbar_try_wait(a, parity)) {
-        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > 4000000000ull) __trap();
+        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > SALE_B200_WAIT_TIMEOUT_NS) __trap();
     }
 }
 
@@ -155,7 +162,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
     const uint64_t t0 = global_timer_ns();
     uint32_t spins = 0;
     while (!mbar_try_wait_cluster(a, parity)) {
-        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > 4000000000ull) __trap();
+        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > SALE_B200_WAIT_TIMEOUT_NS) __trap();
     }
 }
 

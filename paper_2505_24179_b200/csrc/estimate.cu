@@ -5,25 +5,29 @@
 // max_then_dequantize (quant.hpp:170-179) + the relative-score decision and
 // segment OR of selection_pass (selection.hpp:253-271).
 //
-// Work unit (one CTA): one (batch, KV head, <=4 query heads of that GQA group)
-// x one 128-row query tile x a chunk of up to kSegPerUnit middle segments.
+// Work unit (one CTA, two CTAs resident per SM): one (batch, KV head, <=2
+// query heads of that GQA group = kEstHeads) x one 128-row query tile x a
+// chunk of up to kSegPerUnit (64) middle segments.
 //   * The 128-row tile pairs query blocks (2m+1, 2m+2): both have the same
 //     full-segment count F = m-1, so one key range
-//     serves both. A = 4 heads x [128 rows x 128 int8 codes] (64 KB) is loaded
+//     serves both. A = 2 heads x [128 rows x 128 int8 codes] (32 KB) is loaded
 //     once by TMA.
-//   * One stage = one segment = 128 keys (16 KB) through a 6-deep TMA ring.
-//     Every tcgen05.mma has N = 128 (profiles/r1_mma_microbench.txt: an MMA
-//     instruction costs >= 46 cycles whatever its N, so N = 32/64 tiles waste
-//     the tensor core; at N >= 128 i8 runs at 8192 MAC/clk/SM).
-//   * TMEM holds one 128-column accumulator per head; a stage is 4 heads x 4
-//     K-steps of M=128, N=128, K=32, head h into buffer h, so head h's epilogue
-//     has the other three heads' MMAs to drain its buffer, and each K-code
-//     stage is shared by 4 heads (M = 512 rows per byte of K).
-//   * Epilogue (16 warps = 4 lane quadrants x 4 key blocks, thread = row):
-//     tcgen05.ld .pack::16b (|products| <= 128*49 fits int16), 16-bit SIMD max
-//     per 32-key block, est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max,
+//   * One stage = one segment = 128 keys of K codes (16 KB) through a
+//     kEstStages (4) deep TMA ring. Every tcgen05.mma has M = N = 128, K = 32
+//     (profiles/r1_mma_microbench.txt: an MMA instruction costs >= 46 cycles
+//     whatever its N, so N = 32/64 tiles waste the tensor core; at N >= 128 i8
+//     runs at 8192 MAC/clk/SM).
+//   * TMEM: one 128-column int32 accumulator per head (256 columns per CTA,
+//     512 per SM with both CTAs); a stage is 2 heads x 4 K-steps, head h into
+//     buffer h. The two resident CTAs' MMAs interleave on the tensor pipe and
+//     hide each other's issue -> commit -> drain -> release round trip.
+//   * Epilogue (kEpiWarps = 8 warps = 4 lane quadrants x 2 pairs of key
+//     blocks, thread = row): tcgen05.ld .pack::16b (|products| <= 128*49 fits
+//     int16), buffer released right after the load, 16-bit SIMD max per
+//     32-key block, est = ((q_scale * k_scale) * inv_sqrt_d) * (float)max,
 //     est >= fb_row — the reference's float arithmetic. A warp vote ORs rows,
-//     atomicOr ORs segments into the packed mask.
+//     shared-memory atomicOr ORs the rows of the two query blocks, and one
+//     atomicOr per selected segment writes the packed mask.
 #include "common.cuh"
 #include "internal.h"
 
@@ -342,13 +346,8 @@ cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, 
     const int mode = dbg_max ? 1 : (g_est_mode_host == 0 ? 0 : (g_est_mode_host == 2 ? 3 : 2));
     auto kern = mode == 0 ? estimate_kernel<0> : mode == 1 ? estimate_kernel<1>
                                             : mode == 2 ? estimate_kernel<2> : estimate_kernel<3>;
-    static bool configured[4] = {false, false, false, false};
-    if (!configured[mode]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured[mode] = true;
-    }
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
+    if (e != cudaSuccess) return e;
     const int group = hq / hkv;
     const int nsub = (group + kEstHeads - 1) / kEstHeads;
     dim3 grid(static_cast<unsigned>(n_units), static_cast<unsigned>(batch * hkv * nsub));

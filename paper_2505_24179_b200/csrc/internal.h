@@ -16,6 +16,11 @@ namespace sale_b200 {
 int set_error(sale_b200_ctx *ctx, int code, const std::string &msg);
 int ctx_device_of(const sale_b200_ctx *ctx);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the CURRENT
+// device, set once per (device, function): the attribute is per device, so a
+// process driving contexts on several GPUs configures each of them.
+cudaError_t ensure_smem_attr(const void *func, size_t bytes);
+
 struct EstUnit {
     int m;    // 128-row query tile: rows [128m+64, 128m+192) = query blocks 2m+1, 2m+2
     int c;    // chunk of kSegPerUnit middle segments
@@ -50,7 +55,8 @@ cudaError_t attention_profile(int enable, unsigned long long *out16);
 cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, const CUtensorMap &tm_v,
                                     const uint32_t *mask, void *out, int32_t *coverage,
                                     int64_t batch, int64_t tokens, int hq, int hkv, float scale_log2,
-                                    cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1);
+                                    cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1,
+                                    unsigned long long *empty_rows = nullptr);
 
 cudaError_t launch_flop_count(const uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
                               int64_t *counts, cudaStream_t stream);

@@ -21,6 +21,7 @@
 // a warp reads). ~75 KB smem, two CTAs per SM.
 #include "common.cuh"
 #include "exp_table.h"
+#include "internal.h"
 
 #include <cfloat>
 
@@ -376,15 +377,9 @@ cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch,
     if (i_hi < 0 || i_hi > nq) i_hi = nq;
     const int64_t i_first = i_lo > 3 ? i_lo : 3; // blocks with a non-empty middle
     if (i_hi <= i_first) return cudaSuccess;
-    static bool configured = false;
     const size_t smem = sizeof(StatsSmem);
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(sink_local_stats_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(sink_local_stats_kernel), smem);
+    if (e != cudaSuccess) return e;
     dim3 grid(static_cast<unsigned>(i_hi - i_first), static_cast<unsigned>(hq),
               static_cast<unsigned>(batch));
     sink_local_stats_kernel<<<grid, kThreads, smem, stream>>>(

@@ -229,11 +229,55 @@ def pack_mask(cells: np.ndarray, tokens: int) -> np.ndarray:
 
 # ---------------------------------------------------------- stage wrappers
 
-def _shape_of(q, k, head_dim):
+def _check_tensor(name, t, dtype, device=None, ndim=4):
+    """The C ABI takes raw pointers: anything but a contiguous tensor of the
+    expected dtype on the context's device would be read out of bounds or
+    misinterpreted, so it is rejected here (ValueError, like the reference's
+    std::invalid_argument for malformed inputs)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the context on cuda:{device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (e.g. not a head slice of a fused QKV)")
+    if t.dim() != ndim:
+        raise ValueError(f"{name} must have {ndim} dimensions, got {t.dim()}")
+
+
+def _shape_of(q, k, head_dim, v=None, ctx=None):
+    """Validated Shape of q [B,N,Hq,128], k (and v) [B,N,Hkv,128] (bf16,
+    contiguous, on the context's device) — HeadInput::validate
+    (matrix.hpp:66-72) lifted to the batched layout."""
+    import torch
+    dev = (ctx or context()).device
+    for name, t in (("q", q), ("k", k)) + ((("v", v),) if v is not None else ()):
+        _check_tensor(name, t, torch.bfloat16, dev)
     B, N, Hq, P = q.shape
-    if P != HEAD_PITCH:
+    if P != HEAD_PITCH or k.shape[3] != HEAD_PITCH:
         raise ValueError("rows must be padded to 128 elements")
+    if tuple(k.shape[:2]) != (B, N):
+        raise ValueError("HeadInput: key rows must match query rows (batch, tokens)")
+    if v is not None and tuple(v.shape) != tuple(k.shape):
+        raise ValueError("HeadInput: value shape must match key shape")
+    if not 1 <= head_dim <= HEAD_PITCH:
+        raise ValueError("head_dim must be in [1, 128]")
     return Shape(B, N, Hq, k.shape[2], head_dim)
+
+
+def _check_mask(mask, s, ctx=None):
+    import torch
+    if mask is None:
+        return
+    _check_tensor("mask", mask, torch.int32, (ctx or context()).device)
+    nq, _, nw = grid(s.tokens)
+    if tuple(mask.shape) != (s.batch, s.q_heads, nq, nw):
+        raise ValueError(f"mask must be [B, Hq, Nq, W] = {(s.batch, s.q_heads, nq, nw)}, "
+                         f"got {tuple(mask.shape)}")
 
 
 def quantize_qk(q, k, head_dim=128):
@@ -257,6 +301,9 @@ def quantize_per_token(x):
     """quant.hpp:95 for every (batch, head) of x [B,N,H,128]."""
     import torch
     ctx = context()
+    _check_tensor("x", x, torch.bfloat16, ctx.device)
+    if x.shape[3] != HEAD_PITCH:
+        raise ValueError("rows must be padded to 128 elements")
     B, N, H, _ = x.shape
     codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
     scales = torch.empty((B, H, N), dtype=torch.float32, device=x.device)
@@ -269,6 +316,9 @@ def quantize_per_key_block(x):
     """quant.hpp:107 (block_k = 32) for every (batch, head) of x [B,N,H,128]."""
     import torch
     ctx = context()
+    _check_tensor("x", x, torch.bfloat16, ctx.device)
+    if x.shape[3] != HEAD_PITCH:
+        raise ValueError("rows must be padded to 128 elements")
     B, N, H, _ = x.shape
     codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
     scales = torch.empty((B, H, grid(N)[1]), dtype=torch.float32, device=x.device)
@@ -293,6 +343,13 @@ def selection_pass(q, k, q_codes, q_scales, k_codes, k_scales, taus, head_dim=12
     ctx = context()
     s = _shape_of(q, k, head_dim)
     nq, nk, nw = grid(s.tokens)
+    for name, t, dt, shp in (("q_codes", q_codes, torch.int8, tuple(q.shape)),
+                             ("k_codes", k_codes, torch.int8, tuple(k.shape)),
+                             ("q_scales", q_scales, torch.float32, (s.batch, s.q_heads, s.tokens)),
+                             ("k_scales", k_scales, torch.float32, (s.batch, s.kv_heads, nk))):
+        _check_tensor(name, t, dt, ctx.device, len(shp))
+        if tuple(t.shape) != shp:
+            raise ValueError(f"{name} must have shape {shp}, got {tuple(t.shape)}")
     taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (s.q_heads,)))
     mask = torch.empty((s.batch, s.q_heads, nq, nw), dtype=torch.int32, device=q.device)
     dbg_struct = None
@@ -321,7 +378,8 @@ def block_sparse_attention(q, k, v, mask=None, head_dim=128, coverage=False, q_b
     blocks' rows are computed (boundaries 0, nq or odd)."""
     import torch
     ctx = context()
-    s = _shape_of(q, k, head_dim)
+    s = _shape_of(q, k, head_dim, v)
+    _check_mask(mask, s)
     out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
     cov = (torch.empty((s.batch, s.q_heads, s.tokens), dtype=torch.int32, device=q.device)
            if coverage else None)
@@ -345,21 +403,25 @@ def flop_accounting(mask, tokens):
     (computed, skipped, total) causal blocks."""
     import torch
     ctx = context()
+    _check_tensor("mask", mask, torch.int32, ctx.device)
     B, H = mask.shape[0], mask.shape[1]
+    if tuple(mask.shape[2:]) != grid(tokens)[::2]:
+        raise ValueError(f"mask must be [B, Hq, Nq, W] for {tokens} tokens")
     counts = torch.empty((B, H, 3), dtype=torch.int64, device=mask.device)
     ctx._check(ctx.lib.sale_b200_flop_count(ctx.handle, _ptr(mask), B, H, tokens, _ptr(counts),
                                             _stream()))
     return counts
 
 
-def prefill(q, k, v, taus, head_dim=128, mask_out=None, config=None, q_blocks=None):
+def prefill(q, k, v, taus, head_dim=128, mask_out=None, config=None, q_blocks=None, ctx=None):
     """run_pipeline's stage composition (runner.hpp:63-80) on device tensors:
     quantize -> selection -> block-sparse attention. Returns out bf16.
     q_blocks=(i_lo, i_hi): only that query-block range (one GPU's share of a
     split unit, K/V replicated); rows outside it are left untouched."""
     import torch
-    ctx = context()
-    s = _shape_of(q, k, head_dim)
+    ctx = ctx or context()
+    s = _shape_of(q, k, head_dim, v, ctx)
+    _check_mask(mask_out, s, ctx)
     taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (s.q_heads,)))
     out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
     cfg = config if config is not None else default_config()
@@ -381,19 +443,27 @@ def query_block_split(nq, parts):
     grows like i, so the cumulative work like i^2: boundary p sits near
     nq * sqrt(p / parts), rounded to an odd block (the estimator pairs query
     blocks 2m+1, 2m+2). Returns [(i_lo, i_hi), ...] covering [0, nq)."""
+    if parts < 1:
+        raise ValueError("query_block_split: parts must be >= 1")
     bounds = [0]
+    top = nq - 1 if (nq - 1) % 2 == 1 else nq - 2  # largest odd boundary < nq
     for p in range(1, parts):
         x = int(round(nq * (p / parts) ** 0.5)) | 1
+        x = max(x, bounds[-1] + 2 if bounds[-1] > 0 else 1)  # strictly increasing, odd
+        x = min(x, top - 2 * (parts - 1 - p))               # room for the later boundaries
         if bounds[-1] < x < nq:
             bounds.append(x)
     bounds.append(nq)
+    if len(bounds) - 1 != parts:
+        raise ValueError(f"query_block_split: {nq} query blocks cannot be split into {parts} "
+                         "ranges with odd inner boundaries")
     return list(zip(bounds[:-1], bounds[1:]))
 
 
-def prefill_host(q, k, v, taus, out, head_dim=128, config=None):
+def prefill_host(q, k, v, taus, out, head_dim=128, config=None, ctx=None):
     """End to end from host buffers (numpy uint16 / pinned torch bf16 on CPU):
     H2D + the three stages + D2H of out, synchronous."""
-    ctx = context()
+    ctx = ctx or context()
     ptr = (lambda a: C.c_void_p(a.ctypes.data)) if isinstance(q, np.ndarray) else _ptr
     B, N, Hq, _ = q.shape
     s = Shape(B, N, Hq, k.shape[2], head_dim)
@@ -428,7 +498,7 @@ def run_pipeline(q, k, v, taus, config=None, dense_mask=False, head_dim=128):
     index b*Hq+h; "timing" holds device-event stage times of the whole batch,
     label TIMING_LABEL)."""
     ctx = context()
-    s = _shape_of(q, k, head_dim)
+    s = _shape_of(q, k, head_dim, v)
     taus = np.ascontiguousarray(np.broadcast_to(np.asarray(taus, np.float64), (s.q_heads,)))
     cfg = config if config is not None else default_config()
     reps = (HeadReport * (s.batch * s.q_heads))()
@@ -465,7 +535,7 @@ def sweep_thresholds(q, k, v, taus, config=None, head_dim=128):
     """sweep_thresholds (runner.hpp:119-165): rows [{tau, sparsity (mean over
     heads), err (max over heads)}] in the given order."""
     ctx = context()
-    s = _shape_of(q, k, head_dim)
+    s = _shape_of(q, k, head_dim, v)
     taus = np.ascontiguousarray(np.asarray(taus, np.float64).ravel())
     rows = (SweepRow * max(1, len(taus)))()
     cfg = config if config is not None else default_config()
@@ -484,7 +554,14 @@ def calibrate_model(samples, theta=0.4, tau0=0.008, max_halvings=30, config=None
     ctx = context()
     if not samples:
         raise ValueError("calibrate_model: no samples")
-    s = _shape_of(samples[0][0], samples[0][1], head_dim)
+    s = _shape_of(samples[0][0], samples[0][1], head_dim, samples[0][2])
+    for j, smp in enumerate(samples):  # every sample shares the first one's shape
+        if len(smp) != 3:
+            raise ValueError(f"calibrate_model: sample {j} is not a (q, k, v) triple")
+        sj = _shape_of(smp[0], smp[1], head_dim, smp[2])
+        if (sj.batch, sj.tokens, sj.q_heads, sj.kv_heads) != (s.batch, s.tokens, s.q_heads,
+                                                              s.kv_heads):
+            raise ValueError(f"calibrate_model: sample {j} shape differs from sample 0")
     n = len(samples)
     arr = lambda i: (vp * n)(*[C.c_void_p(x[i].data_ptr()) for x in samples])
     st = CalibrationSettings(theta, tau0, max_halvings)

@@ -80,6 +80,25 @@ def test_gqa_workload_extends_reference_heads():
     assert (q16[..., 64:] == 0).all() and (k16[..., 64:] == 0).all()
 
 
+@pytest.mark.parametrize("kind,n,d,hq,hkv", [("sink_local", 300, 128, 8, 2), ("gaussian", 97, 64, 7, 1),
+                                              ("sink_local", 129, 32, 4, 4)])
+def test_gqa_workload_equals_reference_built_generator(kind, n, d, hq, hkv):
+    """The product's GQA generator (workload.cpp) == the same extension built
+    from the reference's own Rng / generators in oracle/_ref
+    (ref_workload_gqa_heads), bit for bit: bench.py's reference arm builds its
+    inputs there without loading the product library."""
+    q16, k16, v16 = sale.workload_gqa(kind, 7, 1, n, hq, hkv, d)
+    q, k, v = (np.empty((hq, n, d), np.float32) for _ in range(3))
+    assert O.REF.ref_workload_gqa_heads(1 if kind == "sink_local" else 0, 7, n, d, hq, hkv, 1, 2,
+                                        q, k, v) == 0
+    f = sale.bf16_bits_to_f32
+    G = hq // hkv
+    for h in range(hq):
+        np.testing.assert_array_equal(q[h], f(q16[0, :, h, :d]))
+        np.testing.assert_array_equal(k[h], f(k16[0, :, h // G, :d]))
+        np.testing.assert_array_equal(v[h], f(v16[0, :, h // G, :d]))
+
+
 def test_sharded_generation_equals_full():
     full = sale.workload_gqa("sink_local", 3, 1, 500, 8, 4, 128)
     for rank in range(2):
@@ -201,13 +220,18 @@ def test_kv_group_sharding_two_ranks_gloo():
 def test_query_block_split_balanced():
     """a unit split across GPUs gets contiguous query-block
     ranges with odd inner boundaries and about equal causal work (~ i^2)."""
-    for nq in (5, 64, 1000, 2048, 4096):
+    for nq, parts in ((3, 3), (4, 4), (8, 8), (1, 2)):
+        with pytest.raises(ValueError):
+            sale.query_block_split(nq, parts)
+    for nq in (5, 17, 64, 1000, 2048, 4096):
         for parts in (1, 2, 3, 4, 8):
+            if parts - 1 > nq // 2:  # odd inner boundaries available in (0, nq)
+                continue
             r = sale.query_block_split(nq, parts)
             assert r[0][0] == 0 and r[-1][1] == nq
             assert all(a < b for a, b in r) and all(r[k][1] == r[k + 1][0] for k in range(len(r) - 1))
             assert all(b % 2 == 1 for _, b in r[:-1])
+            assert len(r) == parts
             if nq >= 1000:
-                assert len(r) == parts
                 work = [(b * b - a * a) / (nq * nq) for a, b in r]
                 assert max(work) - min(work) < 0.02, (nq, parts, work)
