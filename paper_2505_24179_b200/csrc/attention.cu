@@ -453,6 +453,12 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                     tma_load_4d(sm.v[1][st], &tm_v, &sm.v_full[st], 64, g, key0, b);
                 }
             }
+            // drain: the last releases of every ring stage (S / PV commits) land
+            // before the CTA exits, so no mbarrier phase completes unobserved
+            for (int jj = ntiles > kKvStages ? ntiles - kKvStages : 0; jj < ntiles; ++jj)
+                mbar_wait(&sm.k_empty[jj % kKvStages], (jj / kKvStages) & 1);
+            for (int vj = ntiles > kVStages ? ntiles - kVStages : 0; vj < ntiles; ++vj)
+                mbar_wait(&sm.v_empty[vj % kVStages], (vj / kVStages) & 1);
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA

@@ -31,7 +31,7 @@ struct sale_b200_ctx {
     // estimator work-unit table, cached per token count
     EstUnit *d_units = nullptr;
     int64_t units_cap = 0;
-    int64_t units_tokens = -1;
+    std::vector<int64_t> units_key; // tokens + geometry of the cached table
     int64_t n_units = 0;
     // host e2e buffers
     uint8_t *io = nullptr;
@@ -158,8 +158,9 @@ int check_shape(sale_b200_ctx *ctx, const sale_b200_shape *s) {
     return SALE_B200_OK;
 }
 
-// SelectionConfig::validate (selection.hpp:26-37), then the geometry this
-// path is specialised for.
+// SelectionConfig::validate (selection.hpp:26-37), then the block sizes this
+// path is built for (block_q 64, block_k 32: the tile shapes of every kernel).
+// sink_tokens, local_tokens_min and segment_size may take any valid value.
 int check_config(sale_b200_ctx *ctx, const sale_b200_selection_config *c) {
     sale_b200_selection_config d;
     sale_b200_default_config(&d);
@@ -173,12 +174,26 @@ int check_config(sale_b200_ctx *ctx, const sale_b200_selection_config *c) {
                     "SelectionConfig: local_tokens_min must be >= block_k");
     if (c->segment_size < 1)
         return fail(ctx, SALE_B200_INVALID_ARGUMENT, "SelectionConfig: segment_size must be >= 1");
-    if (c->sink_tokens != d.sink_tokens || c->local_tokens_min != d.local_tokens_min ||
-        c->segment_size != d.segment_size || c->block_q != d.block_q || c->block_k != d.block_k)
+    if (c->block_q != kBlockQ || c->block_k != kBlockK)
         return fail(ctx, SALE_B200_UNSUPPORTED,
-                    "the B200 path implements the default SelectionConfig geometry "
-                    "(block_q 64, block_k 32, segment 4, sink 32, local 128)");
+                    "the B200 path implements block_q 64 and block_k 32 (any sink_tokens, "
+                    "local_tokens_min and segment_size)");
+    if (c->segment_size > (1 << 20) || c->local_tokens_min > (1LL << 40) || c->sink_tokens > (1LL << 40))
+        return fail(ctx, SALE_B200_UNSUPPORTED, "SelectionConfig: value out of the supported range");
     return SALE_B200_OK;
+}
+
+// The block-level geometry of a (validated) config for `tokens` tokens
+// (common.cuh Geom; selection.hpp:92-123, :199-202).
+Geom geometry(const sale_b200_selection_config *c, int64_t tokens) {
+    sale_b200_selection_config d;
+    sale_b200_default_config(&d);
+    if (!c) c = &d;
+    Geom g;
+    g.sb = static_cast<int>(cdiv(std::min<int64_t>(c->sink_tokens, tokens), kBlockK));
+    g.nl = static_cast<int>(std::min<int64_t>(cdiv(c->local_tokens_min, kBlockK), 1 << 24));
+    g.seg = static_cast<int>(c->segment_size);
+    return g;
 }
 
 int check_taus(sale_b200_ctx *ctx, const double *taus, int64_t n) {
@@ -231,25 +246,40 @@ int make_map(sale_b200_ctx *ctx, CUtensorMap *map, const void *base, bool bf16, 
     return SALE_B200_OK;
 }
 
-// Work units of the estimator (estimate.cu): every 128-row tile m >= 2 with
-// q-block 2m+1 present, split into chunks of 16 middle segments. Full chunks
-// first (by chunk, then tile: concurrent CTAs share K-code chunks in L2),
-// partial chunks last, largest first.
-int ensure_units(sale_b200_ctx *ctx, int64_t tokens, cudaStream_t stream) {
-    if (ctx->units_tokens == tokens) return SALE_B200_OK;
-    const int64_t nq = cdiv(tokens, kBlockQ);
-    std::vector<EstUnit> units;
-    for (int64_t m = 2; 2 * m + 1 <= nq - 1; ++m) {
-        const int64_t f = m - 1;
-        for (int64_t c = 0; c * kSegPerUnitHost < f; ++c)
-            units.push_back({static_cast<int>(m), static_cast<int>(c),
-                             static_cast<int>(std::min<int64_t>(kSegPerUnitHost, f - c * kSegPerUnitHost))});
-    }
+// Estimator stages (128 keys = 4 key blocks each) of the 128-row tile m =
+// query blocks 2m+1, 2m+2: enough for the larger of their E_i estimated
+// blocks (default geometry: m - 1, one stage per segment).
+int64_t tile_stages(int64_t m, int64_t nq, const Geom &g) {
+    int64_t e = estimated_blocks(2 * m + 1, g);
+    if (2 * m + 2 < nq) e = std::max(e, estimated_blocks(2 * m + 2, g));
+    return (e + kSegment - 1) / kSegment;
+}
+
+// Work units of the estimator (estimate.cu): every 128-row tile with
+// estimated blocks, split into chunks of 64 stages. Full chunks first (by
+// chunk, then tile: concurrent CTAs share K-code chunks in L2), partial chunks
+// last, largest first.
+void append_units(std::vector<EstUnit> &units, int64_t m, int64_t nq, const Geom &g) {
+    const int64_t f = tile_stages(m, nq, g);
+    for (int64_t c = 0; c * kSegPerUnitHost < f; ++c)
+        units.push_back({static_cast<int>(m), static_cast<int>(c),
+                         static_cast<int>(std::min<int64_t>(kSegPerUnitHost, f - c * kSegPerUnitHost))});
+}
+void sort_units(std::vector<EstUnit> &units) {
     std::stable_sort(units.begin(), units.end(), [](const EstUnit &a, const EstUnit &b) {
         if (a.nseg != b.nseg) return a.nseg > b.nseg;
         if (a.c != b.c) return a.c < b.c;
         return a.m < b.m;
     });
+}
+
+int ensure_units(sale_b200_ctx *ctx, int64_t tokens, const Geom &geo, cudaStream_t stream) {
+    const std::vector<int64_t> key = {tokens, geo.sb, geo.nl, geo.seg};
+    if (ctx->units_key == key) return SALE_B200_OK;
+    const int64_t nq = cdiv(tokens, kBlockQ);
+    std::vector<EstUnit> units;
+    for (int64_t m = 0; 2 * m + 1 < nq; ++m) append_units(units, m, nq, geo);
+    sort_units(units);
     const int64_t n = static_cast<int64_t>(units.size());
     if (n > ctx->units_cap) {
         if (ctx->d_units) cudaFree(ctx->d_units);
@@ -261,7 +291,7 @@ int ensure_units(sale_b200_ctx *ctx, int64_t tokens, cudaStream_t stream) {
         SALE_CUDA(ctx, cudaMemcpyAsync(ctx->d_units, units.data(), sizeof(EstUnit) * n,
                                        cudaMemcpyHostToDevice, stream));
     SALE_CUDA(ctx, cudaStreamSynchronize(stream));
-    ctx->units_tokens = tokens;
+    ctx->units_key = key;
     ctx->n_units = n;
     return SALE_B200_OK;
 }
@@ -322,15 +352,15 @@ int upload_taus(sale_b200_ctx *ctx, const double *taus, int64_t n, cudaStream_t 
 
 int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *q_codes,
                 const float *q_scales, const int8_t *k_codes, const float *k_scales,
-                const sale_b200_shape &s, const double *taus, uint32_t *mask, float *thresh,
-                const sale_b200_select_debug *dbg, cudaStream_t stream) {
+                const sale_b200_shape &s, const double *taus, const Geom &geo, uint32_t *mask,
+                float *thresh, const sale_b200_select_debug *dbg, cudaStream_t stream) {
     int st;
     if ((st = upload_taus(ctx, taus, s.q_heads, stream))) return st;
-    if ((st = ensure_units(ctx, s.tokens, stream))) return st;
+    if ((st = ensure_units(ctx, s.tokens, geo, stream))) return st;
     const float isd = inv_sqrt_dim(s.head_dim);
-    SALE_CUDA(ctx, launch_base_mask(mask, s.batch, s.q_heads, s.tokens, stream));
+    SALE_CUDA(ctx, launch_base_mask(mask, s.batch, s.q_heads, s.tokens, geo, stream));
     mark(ctx, 2, stream);
-    SALE_CUDA(ctx, launch_sink_local_stats(q, k, s.batch, s.tokens, s.q_heads, s.kv_heads, isd,
+    SALE_CUDA(ctx, launch_sink_local_stats(q, k, s.batch, s.tokens, s.q_heads, s.kv_heads, isd, geo,
                                            ctx->d_taus, thresh, dbg ? dbg->running_max : nullptr,
                                            dbg ? dbg->exp_sum : nullptr, dbg ? dbg->bound : nullptr,
                                            stream));
@@ -344,8 +374,9 @@ int select_impl(sale_b200_ctx *ctx, const void *q, const void *k, const int8_t *
     if ((st = make_map(ctx, &tm_kc, k_codes, false, s.batch, s.tokens, s.kv_heads, 128, 128))) return st;
     SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_units, ctx->n_units, q_scales, k_scales,
                                    thresh, mask, s.batch, s.tokens, static_cast<int>(s.q_heads),
-                                   static_cast<int>(s.kv_heads), isd,
+                                   static_cast<int>(s.kv_heads), isd, geo,
                                    dbg ? dbg->block_max : nullptr, stream));
+    SALE_CUDA(ctx, launch_segment_or(mask, s.batch, s.q_heads, s.tokens, geo, stream));
     mark(ctx, 4, stream);
     return SALE_B200_OK;
 }
@@ -400,30 +431,23 @@ std::vector<int64_t> chunk_bounds_long(int64_t nq) {
 
 // Estimator units grouped by chunk (tile m belongs to the chunk holding query
 // block 2m+1), each group ordered like the global table.
-int ensure_chunk_units(sale_b200_ctx *ctx, int64_t tokens, const std::vector<int64_t> &bounds,
-                       cudaStream_t stream) {
+int ensure_chunk_units(sale_b200_ctx *ctx, int64_t tokens, const Geom &geo,
+                       const std::vector<int64_t> &bounds, cudaStream_t stream) {
     std::vector<int64_t> key(bounds);
-    key.push_back(tokens);
+    key.insert(key.end(), {tokens, geo.sb, geo.nl, geo.seg});
     if (key == ctx->cunit_key) return SALE_B200_OK;
     const int64_t nq = cdiv(tokens, kBlockQ);
     const size_t nch = bounds.size() - 1;
     std::vector<std::vector<EstUnit>> per(nch);
-    for (int64_t m = 2; 2 * m + 1 <= nq - 1; ++m) {
-        const int64_t f = m - 1;
+    for (int64_t m = 0; 2 * m + 1 < nq; ++m) {
         size_t c = 0;
         while (c + 1 < nch && bounds[c + 1] <= 2 * m + 1) ++c;
-        for (int64_t cc = 0; cc * kSegPerUnitHost < f; ++cc)
-            per[c].push_back({static_cast<int>(m), static_cast<int>(cc),
-                              static_cast<int>(std::min<int64_t>(kSegPerUnitHost, f - cc * kSegPerUnitHost))});
+        append_units(per[c], m, nq, geo);
     }
     std::vector<EstUnit> flat;
     ctx->cunit_off.assign(1, 0);
     for (auto &v : per) {
-        std::stable_sort(v.begin(), v.end(), [](const EstUnit &a, const EstUnit &b) {
-            if (a.nseg != b.nseg) return a.nseg > b.nseg;
-            if (a.c != b.c) return a.c < b.c;
-            return a.m < b.m;
-        });
+        sort_units(v);
         flat.insert(flat.end(), v.begin(), v.end());
         ctx->cunit_off.push_back(static_cast<int64_t>(flat.size()));
     }
@@ -659,8 +683,8 @@ int sale_b200_select(sale_b200_ctx *ctx, const void *q, const void *k, const int
     if ((st = ensure_workspace(ctx, *shape, &w))) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if ((st = ws_begin(ctx, s))) return st;
-    if ((st = select_impl(ctx, q, k, q_codes, q_scales, k_codes, k_scales, *shape, taus, mask_words,
-                          w.thresh, dbg, s)))
+    if ((st = select_impl(ctx, q, k, q_codes, q_scales, k_codes, k_scales, *shape, taus,
+                          geometry(cfg, shape->tokens), mask_words, w.thresh, dbg, s)))
         return st;
     return ws_end(ctx, s);
 }
@@ -714,7 +738,7 @@ int sale_b200_prefill(sale_b200_ctx *ctx, const void *q, const void *k, const vo
                                       shape->kv_heads, s));
     mark(ctx, 1, s);
     if ((st = select_impl(ctx, q, k, w.q_codes, w.q_scales, w.k_codes, w.k_scales, *shape, taus,
-                          mask, w.thresh, nullptr, s)))
+                          geometry(cfg, shape->tokens), mask, w.thresh, nullptr, s)))
         return st;
     // The Selection-Pass always keeps the sink block (selection.hpp:228-232),
     // which every row attends (token 0), so no row can be empty here.
@@ -762,7 +786,8 @@ int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, co
     const size_t grp = i_lo > 0 ? 1 : 0; // the unit group of [i_lo, i_hi)
     if ((st = ws_begin(ctx, s))) return st;
     if ((st = upload_taus(ctx, taus, Hq, s))) return st;
-    if ((st = ensure_chunk_units(ctx, N, bounds, s))) return st;
+    const Geom geo = geometry(cfg, N);
+    if ((st = ensure_chunk_units(ctx, N, geo, bounds, s))) return st;
     const int64_t t0 = i_lo * kBlockQ, t1 = std::min<int64_t>(i_hi * kBlockQ, N);
     mark(ctx, 0, s);
     SALE_CUDA(ctx, launch_quantize_qk(nullptr, k, nullptr, nullptr, w.k_codes, w.k_scales, B, N, Hq,
@@ -771,9 +796,9 @@ int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, co
                                       Hkv, s, t0, t1));
     mark(ctx, 1, s);
     const float isd = inv_sqrt_dim(sh.head_dim);
-    SALE_CUDA(ctx, launch_base_mask(mask, B, Hq, N, s, i_lo, i_hi));
+    SALE_CUDA(ctx, launch_base_mask(mask, B, Hq, N, geo, s, i_lo, i_hi));
     mark(ctx, 2, s);
-    SALE_CUDA(ctx, launch_sink_local_stats(q, k, B, N, Hq, Hkv, isd, ctx->d_taus, w.thresh, nullptr,
+    SALE_CUDA(ctx, launch_sink_local_stats(q, k, B, N, Hq, Hkv, isd, geo, ctx->d_taus, w.thresh, nullptr,
                                            nullptr, nullptr, s, i_lo, i_hi));
     mark(ctx, 3, s);
     const int64_t u0 = ctx->cunit_off[grp], u1 = ctx->cunit_off[grp + 1];
@@ -783,7 +808,8 @@ int sale_b200_prefill_range(sale_b200_ctx *ctx, const void *q, const void *k, co
         if ((st = make_map(ctx, &tm_kc, w.k_codes, false, B, N, Hkv, 128, 128))) return st;
         SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_cunits + u0, u1 - u0, w.q_scales,
                                        w.k_scales, w.thresh, mask, B, N, static_cast<int>(Hq),
-                                       static_cast<int>(Hkv), isd, nullptr, s));
+                                       static_cast<int>(Hkv), isd, geo, nullptr, s));
+        SALE_CUDA(ctx, launch_segment_or(mask, B, Hq, N, geo, s, i_lo, i_hi));
     }
     mark(ctx, 4, s);
     if ((st = attention_impl(ctx, q, k, v, sh, mask, out, nullptr, s, i_lo, i_hi))) return st;
@@ -851,7 +877,8 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
     if ((st = ensure_workspace(ctx, s, &w))) return st;
     if ((st = ws_begin(ctx, s_comp))) return st;
     if ((st = upload_taus(ctx, taus, Hq, s_comp))) return st;
-    if ((st = ensure_chunk_units(ctx, N, bounds, s_comp))) return st;
+    const Geom geo = geometry(cfg, N);
+    if ((st = ensure_chunk_units(ctx, N, geo, bounds, s_comp))) return st;
     CUtensorMap tm_qc, tm_kc;
     if ((st = make_map(ctx, &tm_qc, w.q_codes, false, B, N, Hq, 128, 128))) return st;
     if ((st = make_map(ctx, &tm_kc, w.k_codes, false, B, N, Hkv, 128, 128))) return st;
@@ -883,14 +910,15 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
         SALE_CUDA(ctx, cudaStreamWaitEvent(s_comp, ev[2 * c], 0));
         SALE_CUDA(ctx, launch_quantize_qk(dq, dk, w.q_codes, w.q_scales, w.k_codes, w.k_scales, B, N,
                                           Hq, Hkv, s_comp, t0, t1));
-        SALE_CUDA(ctx, launch_base_mask(w.mask, B, Hq, N, s_comp, i0, i1));
-        SALE_CUDA(ctx, launch_sink_local_stats(dq, dk, B, N, Hq, Hkv, isd, ctx->d_taus, w.thresh,
+        SALE_CUDA(ctx, launch_base_mask(w.mask, B, Hq, N, geo, s_comp, i0, i1));
+        SALE_CUDA(ctx, launch_sink_local_stats(dq, dk, B, N, Hq, Hkv, isd, geo, ctx->d_taus, w.thresh,
                                                nullptr, nullptr, nullptr, s_comp, i0, i1));
         const int64_t u0 = ctx->cunit_off[c], u1 = ctx->cunit_off[c + 1];
         if (u1 > u0)
             SALE_CUDA(ctx, launch_estimate(tm_qc, tm_kc, ctx->d_cunits + u0, u1 - u0, w.q_scales,
                                            w.k_scales, w.thresh, w.mask, B, N, static_cast<int>(Hq),
-                                           static_cast<int>(Hkv), isd, nullptr, s_comp));
+                                           static_cast<int>(Hkv), isd, geo, nullptr, s_comp));
+        SALE_CUDA(ctx, launch_segment_or(w.mask, B, Hq, N, geo, s_comp, i0, i1));
         CUtensorMap tk, tv; // K / V rows [0, t1) of the [B][N][Hkv][128] layout
         if ((st = make_map(ctx, &tk, dk, true, B, N, Hkv, 64, 128, t1))) return st;
         if ((st = make_map(ctx, &tv, dv, true, B, N, Hkv, 64, 128, t1))) return st;

@@ -483,16 +483,48 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Query block i (64 tokens), default geometry:
-// I_SL = {0} U [max(0, 2i-4), frontier]; middle = [1, 2i-4) for i >= 3;
-// full segments F_i = floor((2i-5)/4); the trailing partial run is forced.
+// Selection geometry with block_q = 64, block_k = 32 (selection.hpp:18-38,
+// :92-123, :199-202, :236-245; SURVEY.md Appendix C for the defaults):
+//   sb  = ceil(min(sink_tokens, N) / 32)  sink blocks = the middle's start
+//   nl  = ceil(local_tokens_min / 32)     fully-past blocks of the local window
+//   seg = segment_size
+// Query block i: local window [lo_i, frontier_i], lo_i = max(0, 2i - nl);
+// I_SL = [0, sb) U [lo_i, frontier_i]; middle = [sb, lo_i) when lo_i > sb;
+// full segments F_i = (lo_i - sb) / seg, i.e. E_i = seg * F_i estimated
+// blocks [sb, sb + E_i); the trailing partial run [sb + E_i, lo_i) is forced.
+// Defaults (sb 1, nl 4, seg 4): I_SL = {0} U [2i-4, frontier], F_i =
+// floor((2i-5)/4), middle non-empty from i = 3.
+struct Geom {
+    int sb;  // sink blocks
+    int nl;  // local fully-past blocks
+    int seg; // segment size (blocks)
+};
+
 __host__ __device__ __forceinline__ int64_t frontier_block(int64_t i, int64_t n, int64_t nk) {
     const int64_t qend = (i + 1) * kBlockQ < n ? (i + 1) * kBlockQ : n;
     const int64_t f = (qend - 1) / kBlockK;
     return f < nk - 1 ? f : nk - 1;
 }
-__host__ __device__ __forceinline__ int64_t full_segments(int64_t i) {
-    return i >= 3 ? (2 * i - 5) / kSegment : 0;
+__host__ __device__ __forceinline__ int64_t local_lo(int64_t i, const Geom &g) {
+    const int64_t lo = 2 * i - g.nl;
+    return lo > 0 ? lo : 0;
+}
+__host__ __device__ __forceinline__ bool has_middle(int64_t i, const Geom &g) {
+    return local_lo(i, g) > g.sb;
+}
+// First query block with a non-empty middle region: 2i - nl > sb.
+__host__ __device__ __forceinline__ int64_t first_middle_block(const Geom &g) {
+    return (g.nl + g.sb) / 2 + 1;
+}
+__host__ __device__ __forceinline__ int64_t full_segments(int64_t i, const Geom &g) {
+    return has_middle(i, g) ? (local_lo(i, g) - g.sb) / g.seg : 0;
+}
+// Estimated middle blocks of query block i (E_i = seg * F_i).
+__host__ __device__ __forceinline__ int64_t estimated_blocks(int64_t i, const Geom &g) {
+    return static_cast<int64_t>(g.seg) * full_segments(i, g);
+}
+__host__ __device__ __forceinline__ bool is_default_geom(const Geom &g) {
+    return g.sb == 1 && g.nl == 4 && g.seg == kSegment;
 }
 
 } // namespace sale_b200

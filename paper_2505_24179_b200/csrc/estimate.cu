@@ -55,6 +55,7 @@ struct EstSmem {
     uint64_t tmem_empty[kEstHeads];
     uint32_t tmem_base;
     uint32_t seg_bits[kEstHeads][2][kSegWords];
+    uint32_t blk_bits[kEstHeads][2][kSegment * kSegWords]; // general geometry: per middle block
     float ks[kSegment * kSegPerUnit];
 };
 
@@ -71,13 +72,18 @@ namespace {
 // 3 profiling with the epilogue work skipped. The epilogue's per-head path is
 // latency-critical (every extra instruction there costs issue slack; see
 // profiles/README.md), so the diagnostics are separate instances.
-template <int kMode>
+// kGen: any selection geometry (Geom): the unit's stages start at key block
+// sb, a query block estimates its own E_i blocks, and the epilogue ORs raw
+// per-block decisions into the mask; segment_or_kernel then widens them to
+// segments (segment_aggregate). !kGen: the default geometry, where one stage
+// is exactly one segment and the epilogue writes aggregated segments.
+template <int kMode, bool kGen>
 __global__ void __launch_bounds__(kEstThreads, 2)
 estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_kc,
                 const EstUnit *__restrict__ units, const float *__restrict__ q_scales,
                 const float *__restrict__ k_scales, const float *__restrict__ thresh,
                 uint32_t *__restrict__ mask, int64_t tokens, int hq, int hkv, int nsub,
-                float inv_sqrt_d, int32_t *__restrict__ dbg_max) {
+                float inv_sqrt_d, Geom geo, int32_t *__restrict__ dbg_max) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // dynamic smem base is only 16-B aligned by contract: round up to 1 KB
     EstSmem &sm = *reinterpret_cast<EstSmem *>(smem_raw + smem_pad_1k(smem_raw));
@@ -97,7 +103,7 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
     const int64_t words = (nk + 31) / 32;
     const int nstages = u.nseg;
     const int row0 = 128 * u.m + 64;
-    const int key_base = kBlockK + kStageKeys * kSegPerUnit * u.c; // first key of the unit
+    const int key_base = kBlockK * geo.sb + kStageKeys * kSegPerUnit * u.c; // first key of the unit
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kEstStages; ++s) {
@@ -110,8 +116,10 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
             mbar_init(&sm.tmem_empty[s], kEpiWarps); // all epilogue warps drain every group
         }
         for (int hh = 0; hh < kEstHeads; ++hh)
-            for (int x = 0; x < 2; ++x)
+            for (int x = 0; x < 2; ++x) {
                 for (int w = 0; w < kSegWords; ++w) sm.seg_bits[hh][x][w] = 0;
+                for (int w = 0; w < kSegment * kSegWords; ++w) sm.blk_bits[hh][x][w] = 0;
+            }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<kEstHeads * 128>(&sm.tmem_base);
@@ -209,7 +217,13 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const int64_t jb_base = key_base / kBlockK;
         // the unit's key-block scales, staged once (no global load per stage)
         for (int x = threadIdx.x - 128; x < kSegment * nstages; x += 32 * kEpiWarps)
-            sm.ks[x] = ks_row[jb_base + x];
+            sm.ks[x] = jb_base + x < nk ? ks_row[jb_base + x] : 1.0f;
+        // general geometry: this row's estimated blocks, counted from the
+        // unit's first block (blocks past it are not decided here)
+        const int64_t qi_row = 2 * static_cast<int64_t>(u.m) + 1 + (quad >> 1);
+        const int e_row = kGen ? static_cast<int>(estimated_blocks(qi_row, geo) -
+                                                  static_cast<int64_t>(kSegment) * kSegPerUnit * u.c)
+                               : 0;
         named_bar_sync(1, 32 * kEpiWarps);
         const bool dbg = kMode == 1 && row_ok;
         constexpr bool epi_skip = kMode == 3;
@@ -219,11 +233,17 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         const long long t_epi = clock64();
         // per-row selection flags: bit k of flags[hh][k >> 5] = some column of
         // this row's key block in segment k passed; OR-reduced over rows once
+        // (general geometry: bits 2k, 2k + 1 of gflags[hh][k >> 4] = blocks
+        // 4k + chunk, 4k + chunk + 1 of the unit)
         uint32_t flags[kEstHeads][kSegWords];
+        uint32_t gflags[kEstHeads][kGen ? 2 * kSegWords : 1];
 #pragma unroll
-        for (int hh = 0; hh < kEstHeads; ++hh)
+        for (int hh = 0; hh < kEstHeads; ++hh) {
 #pragma unroll
             for (int w = 0; w < kSegWords; ++w) flags[hh][w] = 0u;
+#pragma unroll
+            for (int w = 0; w < (kGen ? 2 * kSegWords : 1); ++w) gflags[hh][w] = 0u;
+        }
         for (int k = 0; k < nstages; ++k) {
             const float ks = sm.ks[4 * k + chunk], ks1 = sm.ks[4 * k + chunk + 1];
             const uint32_t kbit = 1u << (k & 31);
@@ -266,27 +286,55 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
                                     static_cast<int>(static_cast<int16_t>(v[16] >> 16)));
                 const float est0 = __fmul_rn(__fmul_rn(__fmul_rn(qs[hh], ks), inv_sqrt_d), static_cast<float>(mx0));
                 const float est1 = __fmul_rn(__fmul_rn(__fmul_rn(qs[hh], ks1), inv_sqrt_d), static_cast<float>(mx1));
-                const bool pass = est0 >= fb[hh] || est1 >= fb[hh];
-                flags[hh][0] |= pass ? kb0 : 0u;
-                flags[hh][1] |= pass ? kb1 : 0u;
+                if constexpr (kGen) {
+                    const int jb = 4 * k + chunk; // the unit's block of est0
+                    const uint32_t bits = ((est0 >= fb[hh] && jb < e_row) ? 1u : 0u) |
+                                          ((est1 >= fb[hh] && jb + 1 < e_row) ? 2u : 0u);
+                    const uint32_t sh = static_cast<uint32_t>(2 * (k & 15));
+#pragma unroll
+                    for (int w = 0; w < 2 * kSegWords; ++w) gflags[hh][w] |= (k >> 4) == w ? bits << sh : 0u;
+                } else {
+                    const bool pass = est0 >= fb[hh] || est1 >= fb[hh];
+                    flags[hh][0] |= pass ? kb0 : 0u;
+                    flags[hh][1] |= pass ? kb1 : 0u;
+                }
                 if constexpr (kMode == 1)
                     if (dbg) {
-                        int32_t *dm = dbg_max + ((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk +
-                                      jb_base + 4 * k + chunk;
-                        dm[0] = mx0;
-                        dm[1] = mx1;
+                        const int64_t jb = jb_base + 4 * k + chunk;
+                        int32_t *dm = dbg_max + ((static_cast<int64_t>(b) * hq + h0 + hh) * tokens + tok) * nk + jb;
+                        if (jb < nk) dm[0] = mx0;
+                        if (jb + 1 < nk) dm[1] = mx1;
                     }
             }
         }
         // OR over the warp's 32 rows; the two query blocks of the tile are the
         // lane quadrants {0,1} and {2,3}
+        if constexpr (kGen) {
+            // spread the 2-bit stage groups to nibbles (bits chunk, chunk + 1)
 #pragma unroll
-        for (int hh = 0; hh < kEstHeads; ++hh)
+            for (int hh = 0; hh < kEstHeads; ++hh)
 #pragma unroll
-            for (int w = 0; w < kSegWords; ++w) {
-                const uint32_t any = __reduce_or_sync(0xffffffffu, flags[hh][w]);
-                if (lane == 0 && any && hh < nh) atomicOr(&sm.seg_bits[hh][quad >> 1][w], any);
-            }
+                for (int w = 0; w < 2 * kSegWords; ++w) {
+                    const uint32_t any = __reduce_or_sync(0xffffffffu, gflags[hh][w]);
+                    if (lane == 0 && any && hh < nh)
+#pragma unroll
+                        for (int half16 = 0; half16 < 2; ++half16) {
+                            uint32_t y = (any >> (16 * half16)) & 0xFFFFu;
+                            y = (y | (y << 8)) & 0x00FF00FFu;
+                            y = (y | (y << 4)) & 0x0F0F0F0Fu;
+                            y = (y | (y << 2)) & 0x33333333u;
+                            if (y) atomicOr(&sm.blk_bits[hh][quad >> 1][2 * w + half16], y << chunk);
+                        }
+                }
+        } else {
+#pragma unroll
+            for (int hh = 0; hh < kEstHeads; ++hh)
+#pragma unroll
+                for (int w = 0; w < kSegWords; ++w) {
+                    const uint32_t any = __reduce_or_sync(0xffffffffu, flags[hh][w]);
+                    if (lane == 0 && any && hh < nh) atomicOr(&sm.seg_bits[hh][quad >> 1][w], any);
+                }
+        }
         if (prof && lane == 0) {
             atomicAdd(&g_est_prof[5], static_cast<unsigned long long>(clock64() - t_epi));
             atomicAdd(&g_est_prof[6], static_cast<unsigned long long>(w_epi));
@@ -295,7 +343,19 @@ estimate_kernel(const __grid_constant__ CUtensorMap tm_qc, const __grid_constant
         if (ew == 0 && lane < 2 * kEstHeads) {
             const int h = lane >> 1, half = lane & 1;
             const int64_t qi = 2 * static_cast<int64_t>(u.m) + 1 + half;
-            if (h < nh && qi < nq) {
+            if (kGen && h < nh && qi < nq) {
+                // raw block decisions at blocks sb + 256 c + x (segment_or_kernel widens them)
+                uint32_t *row = mask + ((static_cast<int64_t>(b) * hq + h0 + h) * nq + qi) * words;
+                const int64_t j0 = geo.sb + static_cast<int64_t>(kSegment) * kSegPerUnit * u.c;
+                for (int bw = 0; bw < kSegment * kSegWords; ++bw) {
+                    const uint32_t bits = sm.blk_bits[h][half][bw];
+                    if (!bits) continue;
+                    const int64_t j = j0 + 32 * bw;
+                    const uint32_t w0 = static_cast<uint32_t>(j >> 5), sh = j & 31;
+                    atomicOr(row + w0, bits << sh);
+                    if (sh) atomicOr(row + w0 + 1, bits >> (32 - sh));
+                }
+            } else if (h < nh && qi < nq) {
                 uint32_t *row = mask + ((static_cast<int64_t>(b) * hq + h0 + h) * nq + qi) * words;
                 for (int sw = 0; sw < kSegWords; ++sw) {
                     uint32_t bits = sm.seg_bits[h][half][sw];
@@ -339,20 +399,71 @@ cudaError_t estimate_profile(int enable, unsigned long long *out8) {
 cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
                             int64_t n_units, const float *q_scales, const float *k_scales,
                             const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
-                            int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
+                            int hq, int hkv, float inv_sqrt_d, const Geom &geo, int32_t *dbg_max,
                             cudaStream_t stream) {
     if (n_units == 0) return cudaSuccess;
     const size_t smem = estimate_smem_bytes();
     const int mode = dbg_max ? 1 : (g_est_mode_host == 0 ? 0 : (g_est_mode_host == 2 ? 3 : 2));
-    auto kern = mode == 0 ? estimate_kernel<0> : mode == 1 ? estimate_kernel<1>
-                                            : mode == 2 ? estimate_kernel<2> : estimate_kernel<3>;
+    using Kern = decltype(&estimate_kernel<0, false>);
+    Kern kern;
+    if (is_default_geom(geo))
+        kern = mode == 0 ? estimate_kernel<0, false> : mode == 1 ? estimate_kernel<1, false>
+             : mode == 2 ? estimate_kernel<2, false> : estimate_kernel<3, false>;
+    else
+        kern = mode == 1 ? estimate_kernel<1, true> : estimate_kernel<0, true>;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
     if (e != cudaSuccess) return e;
     const int group = hq / hkv;
     const int nsub = (group + kEstHeads - 1) / kEstHeads;
     dim3 grid(static_cast<unsigned>(n_units), static_cast<unsigned>(batch * hkv * nsub));
     kern<<<grid, kEstThreads, smem, stream>>>(tm_qc, tm_kc, units, q_scales, k_scales, thresh, mask,
-                                              tokens, hq, hkv, nsub, inv_sqrt_d, dbg_max);
+                                              tokens, hq, hkv, nsub, inv_sqrt_d, geo, dbg_max);
+    return cudaGetLastError();
+}
+
+namespace {
+// segment_aggregate (selection.hpp:182-195) over the raw per-block decisions
+// the general-geometry estimator wrote: full segment s of query block i
+// (blocks [sb + seg s, sb + seg (s + 1)), s < F_i) is selected iff any of its
+// blocks is, so a selected segment only gains bits — OR-ing its full range
+// touches no other segment's bits, and lanes can work on segments
+// independently. One warp per mask row.
+__global__ void __launch_bounds__(256)
+segment_or_kernel(uint32_t *__restrict__ mask, int64_t rows, int64_t nq, int64_t words, Geom geo,
+                  int64_t i_lo, int64_t ni) {
+    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= rows * ni) return;
+    const int64_t bh = wid / ni, i = i_lo + wid % ni;
+    const int64_t F = full_segments(i, geo);
+    uint32_t *row = mask + (bh * nq + i) * words;
+    for (int64_t s = lane; s < F; s += 32) {
+        const int64_t a = geo.sb + static_cast<int64_t>(geo.seg) * s, e = a + geo.seg; // [a, e)
+        bool any = false;
+        for (int64_t w = a >> 5; w <= (e - 1) >> 5 && !any; ++w) {
+            const int64_t lo = w * 32 > a ? w * 32 : a, hi = (w + 1) * 32 < e ? (w + 1) * 32 : e;
+            const uint32_t m = (0xFFFFFFFFu >> (32 - (hi - lo))) << (lo - w * 32);
+            any = (row[w] & m) != 0u;
+        }
+        if (!any) continue;
+        for (int64_t w = a >> 5; w <= (e - 1) >> 5; ++w) {
+            const int64_t lo = w * 32 > a ? w * 32 : a, hi = (w + 1) * 32 < e ? (w + 1) * 32 : e;
+            atomicOr(row + w, (0xFFFFFFFFu >> (32 - (hi - lo))) << (lo - w * 32));
+        }
+    }
+}
+} // namespace
+
+cudaError_t launch_segment_or(uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
+                              const Geom &geo, cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
+    if (is_default_geom(geo)) return cudaSuccess; // the estimator wrote whole segments
+    const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
+    const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
+    if (i_hi < 0 || i_hi > nq) i_hi = nq;
+    if (i_hi <= i_lo) return cudaSuccess;
+    const int64_t warps = batch * hq * (i_hi - i_lo);
+    segment_or_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, stream>>>(
+        mask, batch * hq, nq, (nk + 31) / 32, geo, i_lo, i_hi - i_lo);
     return cudaGetLastError();
 }
 

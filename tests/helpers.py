@@ -53,7 +53,7 @@ def oracle_quant(inp: Inputs):
     return qq, kq
 
 
-def oracle_select(inp: Inputs, taus, qq=None, kq=None, debug=False, heads=None):
+def oracle_select(inp: Inputs, taus, qq=None, kq=None, debug=False, heads=None, geom=None):
     qq, kq = (qq, kq) if qq is not None else oracle_quant(inp)
     taus = np.broadcast_to(np.asarray(taus, np.float64), (inp.Hq,))
     heads = heads or inp.heads()
@@ -61,8 +61,10 @@ def oracle_select(inp: Inputs, taus, qq=None, kq=None, debug=False, heads=None):
     def one(i):
         b, h = heads[i]
         g = h // inp.G
+        sink, local, seg = geom or (32, 128, 4)
         return O.selection_pass(inp.qh(b, h), inp.kh(b, g), *qq[(b, h)], *kq[(b, g)],
-                                c=O.cfg(tau=float(taus[h])), debug=debug)
+                                c=O.cfg(tau=float(taus[h]), sink_tokens=sink, local_tokens_min=local,
+                                        segment_size=seg), debug=debug)
 
     res = O.map_heads(one, len(heads))
     return dict(zip(heads, res))

@@ -60,6 +60,7 @@ def _ulp_diff(a, b):
 def _report(name, rep):
     """Margin report: a pytest warning (shown in the -q summary) and a JSON
     file next to the GPU run's other outputs."""
+    rep = {k: (v.item() if hasattr(v, "item") else v) for k, v in rep.items()}
     warnings.warn(f"{name}: {json.dumps(rep)}", UserWarning)
     out = os.environ.get("SALE_REPORT_DIR", "gpurun_out")
     if os.path.isdir(out):

@@ -101,18 +101,33 @@ def test_quantize_hand_rows(torch):
 
 # ------------------------------------------------------------------ stage 2
 
-def _check_selection(inp, taus, dbg_check=True):
+def _check_selection(inp, taus, dbg_check=True, geom=None):
+    """geom = (sink_tokens, local_tokens_min, segment_size) with blocks 64/32,
+    or None for the default SelectionConfig."""
     import torch
     q, k, _ = inp.torch()
+    sink, local, seg = geom or (32, 128, 4)
+    cfg = sale.SelectionConfig(sink, local, seg, 64, 32)
     qc, qs, kc, ks = sale.quantize_qk(q, k, inp.d)
-    mask, dbg = sale.selection_pass(q, k, qc, qs, kc, ks, taus, inp.d, debug=True)
+    mask, dbg = sale.selection_pass(q, k, qc, qs, kc, ks, taus, inp.d, config=cfg, debug=True)
     torch.cuda.synchronize()
     cells = sale.unpack_mask(_to_np(mask), inp.N)
-    ref = oracle_select(inp, taus, debug=True)
+    ref = oracle_select(inp, taus, debug=True, geom=geom)
     m, l, bound, bmax = (_to_np(x) for x in (dbg.running_max, dbg.exp_sum, dbg.bound,
                                              dbg.block_max))
+    # the B200 path estimates the full segments only: the trailing partial run
+    # is forced on by segment_aggregate (selection.hpp:188) whatever its
+    # estimate, so its products are never needed.
+    nq, nk, _ = sale.grid(inp.N)
+    sb = -(-min(sink, inp.N) // 32)
+    nl = -(-local // 32)
+    i = np.arange(inp.N) // 64
+    lo = np.maximum(2 * i - nl, 0)
+    E = np.where(lo > sb, seg * ((lo - sb) // seg), 0)
+    j = np.arange(nk)[None, :]
+    est_blocks = (j >= sb) & (j < sb + E[:, None])
     for (b, h), (rmask, rdbg) in ref.items():
-        np.testing.assert_array_equal(cells[b, h], rmask, err_msg=f"mask b={b} h={h}")
+        np.testing.assert_array_equal(cells[b, h], rmask, err_msg=f"mask b={b} h={h} geom={geom}")
         if not dbg_check:
             continue
         est = ~np.isnan(rdbg["m"])
@@ -120,18 +135,46 @@ def _check_selection(inp, taus, dbg_check=True):
         # exp_sum: table-driven double exp (~0.5 ulp) vs glibc -> allow 2 ulp
         np.testing.assert_allclose(l[b, h][est], rdbg["l"][est], rtol=4.5e-16, atol=0)
         np.testing.assert_allclose(bound[b, h][est], rdbg["bound"][est], rtol=1e-15, atol=1e-15)
-        # the B200 path estimates the full segments only: the trailing partial
-        # run is forced on by segment_aggregate (selection.hpp:188) whatever
-        # its estimate, so its products are never needed.
-        nq, nk, _ = sale.grid(inp.N)
-        i = np.arange(inp.N) // 64
-        full = np.where(i >= 3, (2 * i - 5) // 4, 0)
-        j = np.arange(nk)[None, :]
-        est_blocks = (j >= 1) & (j < 1 + 4 * full[:, None])
         ok = (rdbg["block_max"] != np.iinfo(np.int32).min) & est_blocks
         assert ok.sum() == est_blocks.sum()
         np.testing.assert_array_equal(bmax[b, h][ok], rdbg["block_max"][ok])
     return cells, ref
+
+
+@pytest.mark.parametrize("geom,N,seed", [((1, 32, 1), 1000, 1), ((40, 95, 5), 2048, 2),
+                                         ((64, 128, 4), 1536, 3), ((300, 700, 9), 4096, 4),
+                                         ((33, 256, 2), 3000, 5), ((1, 33, 3), 777, 6),
+                                         ((200, 64, 7), 2500, 7), ((32, 128, 1), 2048, 8)])
+def test_selection_general_geometry(torch, geom, N, seed):
+    """Non-default sink_tokens / local_tokens_min / segment_size with the
+    64/32 blocks (selection.hpp:18-38, :92-123, :182-195): masks, statistics
+    and estimated block maxima against the oracle; then the sparse pass, the
+    one-shot prefill, query-block ranges and the chunked host pipeline on
+    the same geometry."""
+    inp = Inputs("sink_local" if seed % 2 else "gaussian", 40 + seed, 1, N, 4, 2)
+    taus = [0.004, 0.05, 0.0005, 0.02]
+    cells, _ = _check_selection(inp, taus, geom=geom)
+    q, k, v = inp.torch()
+    cfg = sale.SelectionConfig(*geom, 64, 32)
+    nq, nk, nw = sale.grid(N)
+    pm = torch.empty((1, 4, nq, nw), dtype=torch.int32, device="cuda")
+    out = sale.prefill(q, k, v, taus, mask_out=pm, config=cfg)
+    np.testing.assert_array_equal(sale.unpack_mask(_to_np(pm), N), cells)
+    ref = _oracle_attention(inp, cells, inp.heads())
+    outf = _to_np(out.float())
+    for (b, h), (o, rcov, st) in ref.items():
+        assert st == 0
+        got = outf[b, :, h, :inp.d]
+        assert max_abs(got, o) < ATOL_MAX and mean_abs(got, o) < ATOL_MEAN
+    for r in sale.query_block_split(nq, 2):
+        part = torch.zeros_like(pm)
+        po = sale.prefill(q, k, v, taus, mask_out=part, config=cfg, q_blocks=r)
+        assert torch.equal(part[:, :, r[0]:r[1]], pm[:, :, r[0]:r[1]])
+        t0, t1 = 64 * r[0], min(64 * r[1], N)
+        assert torch.equal(po[:, t0:t1].view(torch.int16), out[:, t0:t1].view(torch.int16))
+    host = np.empty_like(inp.q16)
+    sale.prefill_host(inp.q16, inp.k16, inp.v16, taus, host, config=cfg)
+    assert np.array_equal(host, out.cpu().view(torch.int16).numpy().view(np.uint16))
 
 
 @pytest.mark.parametrize("N", [2048, 1000, 200])
@@ -379,6 +422,6 @@ def test_invalid_arguments(torch):
     with pytest.raises(ValueError):
         sale.selection_pass(q, k, qc, qs, kc, ks, 0.004, config=cfg)
     cfg = sale.default_config()
-    cfg.block_q = 32
+    cfg.block_q = 32  # only the 64 / 32 blocks are implemented
     with pytest.raises(NotImplementedError):
         sale.selection_pass(q, k, qc, qs, kc, ks, 0.004, config=cfg)
