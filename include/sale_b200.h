@@ -28,9 +28,10 @@
  *   mask_words   u32  [B][Hq][ceil(N/64)][ceil(ceil(N/32)/32)] packed BlockMask
  *                (bit j%32 of word j/32 of row i == BlockMask::get(i, j))
  *   out          bf16 [B][N][Hq][128]
- * Geometry: the reference's default SelectionConfig (selection.hpp:18-24):
- * block_q 64, block_k 32, segment 4, sink 32 tokens, local >= 128 tokens; Hq a
- * multiple of Hkv (GQA); head_dim <= 128 (the row pitch is always 128).
+ * Geometry: block_q 64 and block_k 32 (the reference's defaults,
+ * selection.hpp:22-23; other block sizes return SALE_B200_UNSUPPORTED) with any
+ * valid sink_tokens, local_tokens_min and segment_size (defaults 32 / 128 / 4);
+ * Hq a multiple of Hkv (GQA); head_dim <= 128 (the row pitch is always 128).
  *
  * Streams: every call is stream-ordered and asynchronous unless it says
  * otherwise; `stream` is a cudaStream_t (NULL = legacy default stream).

@@ -158,8 +158,13 @@ int main() {
                             config.tau);
             const SparseAttentionOutput so = block_sparse_attention(input, ref, grid);
             const SparseAttentionOutput sg = b200::block_sparse_attention(input, got, grid);
+            // the drop-in returns bf16 outputs: compare with the reference's
+            // output rounded to bf16 (with d as small as 4 and rows attending a
+            // handful of keys, |o| ~ 1 and the storage rounding alone is ~1e-3)
+            DenseMatrix ref_bf16 = so.output;
+            for (float &x : ref_bf16.data()) x = bf16_round(x);
             double mean = 0.0;
-            const double worst = max_abs_diff(so.output, sg.output, &mean);
+            const double worst = max_abs_diff(ref_bf16, sg.output, &mean);
             CHECK(worst < 2e-2 && mean < 1e-3);
             if (!(worst < 2e-2 && mean < 1e-3))
                 std::printf("  geometry trial %d/%d: n=%zu d=%zu max %g mean %g\n", series, trial, n, d,
