@@ -50,6 +50,7 @@ struct StatsSmem {
     } u;
     double bmax[kRows][kMaxSlBlocks];          // block max, then running max
     double bsum[kRows][kMaxSlBlocks];          // per-block exp sums
+    double escale[kRows][kMaxSlBlocks];        // exp(m_old - m_new) of each block's l update
     double carry[3][kRows];                    // per row across I_SL chunks: running max, m_old, l
     int blk_len[kMaxSlBlocks];
     double2 exp_tab[256];                      // {hi, lo} of 2^(j/256)
@@ -329,6 +330,11 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
                     sum = __dadd_rn(sum, exp_nonpos(static_cast<double>(lg[t]) - m_new, sm.exp_tab));
             }
             sm.bsum[r][sl] = sum;
+            // the rescale factor of this block's l update, exp(m_old - m_new)
+            // (m_old = the running max before the block), computed here in
+            // parallel instead of in the sequential per-row combine
+            const double m_old = sl == 0 ? sm.carry[1][r] : sm.bmax[r][sl - 1];
+            sm.escale[r][sl] = exp_nonpos(m_old - m_new, sm.exp_tab);
         }
         __syncthreads();
         SALE_PHASE(6)
@@ -336,9 +342,8 @@ sink_local_stats_kernel(const __nv_bfloat16 *__restrict__ q, const __nv_bfloat16
         if (tid < qrows) {
             double m_old = sm.carry[1][tid], l_run = sm.carry[2][tid];
             for (int sl = 0; sl < cn; ++sl) {
-                const double m_new = sm.bmax[tid][sl];
-                l_run = __dadd_rn(__dmul_rn(l_run, exp_nonpos(m_old - m_new, sm.exp_tab)), sm.bsum[tid][sl]);
-                m_old = m_new;
+                l_run = __dadd_rn(__dmul_rn(l_run, sm.escale[tid][sl]), sm.bsum[tid][sl]);
+                m_old = sm.bmax[tid][sl];
             }
             sm.carry[1][tid] = m_old;
             sm.carry[2][tid] = l_run;
