@@ -39,7 +39,7 @@ struct sale_b200_ctx {
     cudaStream_t io_stream = nullptr;
     // chunked host pipeline (sale_b200_prefill_host): compute and D2H streams,
     // per-chunk estimator units grouped by chunk
-    cudaStream_t comp_stream = nullptr, out_stream = nullptr;
+    cudaStream_t comp_stream = nullptr, out_stream = nullptr, attn_stream = nullptr;
     EstUnit *d_cunits = nullptr;
     size_t cunits_bytes = 0;
     std::vector<int64_t> cunit_key;
@@ -620,6 +620,7 @@ void sale_b200_ctx_destroy(sale_b200_ctx *ctx) {
     if (ctx->io_stream) cudaStreamDestroy(ctx->io_stream);
     if (ctx->comp_stream) cudaStreamDestroy(ctx->comp_stream);
     if (ctx->out_stream) cudaStreamDestroy(ctx->out_stream);
+    if (ctx->attn_stream) cudaStreamDestroy(ctx->attn_stream);
     if (ctx->d_cunits) cudaFree(ctx->d_cunits);
     if (ctx->ws_ev) cudaEventDestroy(ctx->ws_ev);
     if (ctx->d_empty) cudaFree(ctx->d_empty);
@@ -856,13 +857,18 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
         ctx->io_bytes = need;
         SALE_CUDA(ctx, cudaMemset(ctx->io, 0, need));
     }
-    for (cudaStream_t *p : {&ctx->io_stream, &ctx->comp_stream, &ctx->out_stream})
+    for (cudaStream_t *p : {&ctx->io_stream, &ctx->comp_stream, &ctx->out_stream, &ctx->attn_stream})
         if (!*p) SALE_CUDA(ctx, cudaStreamCreateWithFlags(p, cudaStreamNonBlocking));
     uint8_t *dq = ctx->io, *dk = dq + align256(qbytes), *dv = dk + align256(kbytes),
             *dout = dv + align256(kbytes);
-    cudaStream_t s_in = ctx->io_stream, s_comp = ctx->comp_stream, s_out = ctx->out_stream;
-    // The prefill in token chunks, three streams: the H2D copy of chunk c+1 and
-    // the D2H copy of chunk c-1 run under chunk c's kernels. Every stage reads
+    cudaStream_t s_in = ctx->io_stream, s_comp = ctx->comp_stream, s_out = ctx->out_stream,
+                 s_attn = ctx->attn_stream;
+    // The prefill in token chunks on four streams: the H2D copies (s_in) run
+    // ahead; the Selection-Pass of chunk c (K1, base mask, K2a, K2b: s_comp)
+    // waits for chunk c's copy; the attention of chunk c (s_attn) waits for
+    // its mask, so it overlaps the Selection-Pass of chunk c+1 (their CTAs
+    // fill each other's tail waves); the D2H of chunk c (s_out) follows its
+    // attention. Every stage reads
     // only data of its own and earlier chunks (causal): the attention's last
     // 128-key K / V tile may extend past the chunk end t1 (into rows the H2D of
     // chunk c+1 is still writing), so chunk c's K / V tensor maps end at t1 and
@@ -884,7 +890,7 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
     if ((st = make_map(ctx, &tm_kc, w.k_codes, false, B, N, Hkv, 128, 128))) return st;
     const float isd = inv_sqrt_dim(s.head_dim);
     const float scale_log2 = isd * 1.4426950408889634f;
-    std::vector<cudaEvent_t> ev(2 * nch);
+    std::vector<cudaEvent_t> ev(3 * nch); // per chunk: copied in, selected, attended
     for (auto &e : ev) SALE_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     struct EvFree {
         std::vector<cudaEvent_t> &e;
@@ -906,8 +912,8 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
         SALE_CUDA(ctx, copy_rows(dq, q, Hq, t0, t1, cudaMemcpyHostToDevice, s_in));
         SALE_CUDA(ctx, copy_rows(dk, k, Hkv, t0, t1, cudaMemcpyHostToDevice, s_in));
         SALE_CUDA(ctx, copy_rows(dv, v, Hkv, t0, t1, cudaMemcpyHostToDevice, s_in));
-        SALE_CUDA(ctx, cudaEventRecord(ev[2 * c], s_in));
-        SALE_CUDA(ctx, cudaStreamWaitEvent(s_comp, ev[2 * c], 0));
+        SALE_CUDA(ctx, cudaEventRecord(ev[3 * c], s_in));
+        SALE_CUDA(ctx, cudaStreamWaitEvent(s_comp, ev[3 * c], 0));
         SALE_CUDA(ctx, launch_quantize_qk(dq, dk, w.q_codes, w.q_scales, w.k_codes, w.k_scales, B, N,
                                           Hq, Hkv, s_comp, t0, t1));
         SALE_CUDA(ctx, launch_base_mask(w.mask, B, Hq, N, geo, s_comp, i0, i1));
@@ -919,17 +925,20 @@ int sale_b200_prefill_host(sale_b200_ctx *ctx, const uint16_t *q, const uint16_t
                                            w.k_scales, w.thresh, w.mask, B, N, static_cast<int>(Hq),
                                            static_cast<int>(Hkv), isd, geo, nullptr, s_comp));
         SALE_CUDA(ctx, launch_segment_or(w.mask, B, Hq, N, geo, s_comp, i0, i1));
+        SALE_CUDA(ctx, cudaEventRecord(ev[3 * c + 1], s_comp));
+        SALE_CUDA(ctx, cudaStreamWaitEvent(s_attn, ev[3 * c + 1], 0));
         CUtensorMap tk, tv; // K / V rows [0, t1) of the [B][N][Hkv][128] layout
         if ((st = make_map(ctx, &tk, dk, true, B, N, Hkv, 64, 128, t1))) return st;
         if ((st = make_map(ctx, &tv, dv, true, B, N, Hkv, 64, 128, t1))) return st;
         SALE_CUDA(ctx, launch_sparse_attention(dq, tk, tv, w.mask, dout, nullptr, B, N,
                                                static_cast<int>(Hq), static_cast<int>(Hkv),
-                                               scale_log2, s_comp, i0, i1));
-        SALE_CUDA(ctx, cudaEventRecord(ev[2 * c + 1], s_comp));
-        SALE_CUDA(ctx, cudaStreamWaitEvent(s_out, ev[2 * c + 1], 0));
+                                               scale_log2, s_attn, i0, i1));
+        SALE_CUDA(ctx, cudaEventRecord(ev[3 * c + 2], s_attn));
+        SALE_CUDA(ctx, cudaStreamWaitEvent(s_out, ev[3 * c + 2], 0));
         SALE_CUDA(ctx, copy_rows(out, dout, Hq, t0, t1, cudaMemcpyDeviceToHost, s_out));
     }
     SALE_CUDA(ctx, cudaStreamSynchronize(s_out));
+    SALE_CUDA(ctx, cudaStreamSynchronize(s_attn));
     SALE_CUDA(ctx, cudaStreamSynchronize(s_comp));
     return ws_end(ctx, s_comp);
 }

@@ -42,9 +42,15 @@ def torch():
     return t
 
 
-@pytest.fixture(scope="module")
-def llama32k():
-    return Inputs("sink_local", 7, 1, 32768, 32, 8)
+_INPUTS = {}
+
+
+def _inputs(hq, hkv):
+    """32K-token GQA sink-local inputs (seed 7), cached per shape."""
+    if (hq, hkv) not in _INPUTS:
+        _INPUTS.clear()
+        _INPUTS[(hq, hkv)] = Inputs("sink_local", 7, 1, 32768, hq, hkv)
+    return _INPUTS[(hq, hkv)]
 
 
 def _np(t):
@@ -91,9 +97,12 @@ def _oracle_head(inp, b, h, tau, want_block_max=False):
     return dict(qc=qc, qs=qs, kc=kc, ks=ks, m=m, l=l, bound=bound, mask=mask, rep=rep)
 
 
-@pytest.mark.parametrize("tau", [0.004, 0.064])
-def test_c2_gate_32k_all_heads(torch, llama32k, tau):
-    inp = llama32k
+@pytest.mark.parametrize("model,hq,hkv,tau", [("llama", 32, 8, 0.004), ("llama", 32, 8, 0.064),
+                                              ("qwen", 28, 4, 0.004)])
+def test_c2_gate_32k_all_heads(torch, model, hq, hkv, tau):
+    """Llama-3.1-8B (configs[1]) and the Qwen2.5-7B shape (G = 7, configs[3]'s
+    head layout) at 32K: every head, every query block."""
+    inp = _inputs(hq, hkv)
     N, Hq, Hkv = inp.N, inp.Hq, inp.Hkv
     q, k, v = inp.torch()
     nq, nk, nw = sale.grid(N)
@@ -106,7 +115,7 @@ def test_c2_gate_32k_all_heads(torch, llama32k, tau):
     qc, qs, kc, ks = (_np(x) for x in (qc, qs, kc, ks))
     cells = sale.unpack_mask(_np(mask), N)
     # ---- debug instance for two KV groups (8 q heads): stats + block maxima
-    dbg_groups = (0, 5)
+    dbg_groups = (0, Hkv - 1)
     dbg = {}
     for g in dbg_groups:
         hs = slice(g * inp.G, (g + 1) * inp.G)
@@ -149,7 +158,7 @@ def test_c2_gate_32k_all_heads(torch, llama32k, tau):
                     bmax[r, 64 * i:64 * i + 64, 1:1 + est_blocks], bm[:, :est_blocks],
                     err_msg=f"block max h={h} i={i}")
     # ---- the BLAS restatement itself against oracle_selection_pass (2 heads)
-    for h in (0, 31):
+    for h in (0, Hq - 1):
         qh, kh = inp.qh(0, h), inp.kh(0, h // inp.G)
         o = orc[h]
         ref = O.selection_pass(qh, kh, o["qc"], o["qs"], o["kc"], o["ks"], c=O.cfg(tau=tau))
@@ -164,15 +173,16 @@ def test_c2_gate_32k_all_heads(torch, llama32k, tau):
         err = np.abs(outf[0, :, h, :128].astype(np.float64) - ref)
         return float(err.max()), float(err.mean())
 
-    errs = O.map_heads(lambda x: attn((0, 9, 22, 31)[x]), 4, threads=4)
-    for (mx, mn), h in zip(errs, (0, 9, 22, 31)):
+    out_heads = (0, 9, Hq - 10, Hq - 1)
+    errs = O.map_heads(lambda x: attn(out_heads[x]), 4, threads=4)
+    for (mx, mn), h in zip(errs, out_heads):
         assert mx < ATOL_MAX and mn < ATOL_MEAN, (h, mx, mn)
     rep = _merge([o["rep"] for o in orc])
     rep.update(tokens=N, heads=Hq, tau=tau, max_abs_err=max(e[0] for e in errs),
                mean_abs_err=max(e[1] for e in errs),
                density=float(cells[0].sum() / (Hq * sum(2 * i + 2 for i in range(nq)))))
     assert rep["near_ties"] == 0 and rep["min_decision_rel"] > 1e-12, rep
-    _report(f"c2_32k_tau{tau}", rep)
+    _report(f"c2_32k_{model}_tau{tau}", rep)
 
 
 def test_c2_extension_128k_four_heads_all_query_blocks(torch):
