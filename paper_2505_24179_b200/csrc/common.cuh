@@ -438,6 +438,16 @@ __device__ __forceinline__ void tmem_st16x128_x16(uint32_t taddr, const uint32_t
         : "memory");
 }
 
+// 16x128b.x8: 16 lanes x 32 columns; thread T: lanes T/4, T/4+8 at column
+// 4R + T%4: r[2R + (second lane)], R < 8.
+__device__ __forceinline__ void tmem_st16x128_x8(uint32_t taddr, const uint32_t *r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16};" ::"r"(taddr),
+        SALE_W16(r, 0)
+        : "memory");
+}
+
 // 16x256b.x1: 16 lanes x 8 columns, thread T: lanes T/4, T/4+8 at columns
 // 2(T%4) + e: r[2 * (second lane) + e].
 __device__ __forceinline__ void tmem_ld16x256_x1(uint32_t taddr, uint32_t *r) {

@@ -164,66 +164,6 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
     tmem_ld16x256_x16(sAddr, s);
     tmem_ld_wait();
     const bool full = nib == 0xFu && lim0 >= 127 && lim1 >= 127;
-    const unsigned long long sc2 = pack_f2(scale_log2, scale_log2);
-    if (__all_sync(0xffffffffu, full && st.m[0] != -INFINITY && st.m[1] != -INFINITY)) {
-        // Speculative path (full tiles once both rows have a reference): P is
-        // computed against the running references right away, interleaved
-        // with the row max instead of after it; when no row max grows by > 8
-        // (the usual case) the references stay and P is exactly what the
-        // in-order path computes. Otherwise S is reloaded and the tile takes
-        // the in-order path below.
-        const unsigned long long nmf[2] = {pack_f2(-st.m[0], -st.m[0]), pack_f2(-st.m[1], -st.m[1])};
-        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int R = 0; R < 16; ++R)
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                mx[2 * k + (R & 1)] =
-                    fmax3(mx[2 * k + (R & 1)], __uint_as_float(s[4 * R + 2 * k]), __uint_as_float(s[4 * R + 2 * k + 1]));
-                unsigned long long x =
-                    (static_cast<unsigned long long>(s[4 * R + 2 * k + 1]) << 32) | s[4 * R + 2 * k];
-                ffma2_f32(x, sc2, nmf[k]);
-                float p0, p1;
-                if ((R & 7) == 0 || (R & 7) == 3 || (R & 7) == 5) {
-                    const unsigned long long xc =
-                        pack_f2(fmaxf(__uint_as_float(static_cast<uint32_t>(x)), -125.0f),
-                                fmaxf(__uint_as_float(static_cast<uint32_t>(x >> 32)), -125.0f));
-                    unsigned long long t = xc;
-                    fadd2_f32(t, pack_f2(12582912.0f, 12582912.0f));
-                    unsigned long long r = t;
-                    fadd2_f32(r, pack_f2(-12582912.0f, -12582912.0f));
-                    unsigned long long f = xc;
-                    fsub2_f32(f, r);
-                    unsigned long long pp = pack_f2(0.05592204f, 0.05592204f);
-                    ffma2_f32(pp, f, pack_f2(0.24264008f, 0.24264008f));
-                    ffma2_f32(pp, f, pack_f2(0.69312102f, 0.69312102f));
-                    ffma2_f32(pp, f, pack_f2(0.99992448f, 0.99992448f));
-                    p0 = __uint_as_float(shl23_add(static_cast<uint32_t>(t), static_cast<uint32_t>(pp)));
-                    p1 = __uint_as_float(shl23_add(static_cast<uint32_t>(t >> 32),
-                                                   static_cast<uint32_t>(pp >> 32)));
-                } else {
-                    p0 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x)));
-                    p1 = ex2_approx(__uint_as_float(static_cast<uint32_t>(x >> 32)));
-                }
-                s[2 * R + k] = pack_bf16x2(p0, p1); // index 2R+k was already consumed
-            }
-        float u0 = fmaxf(mx[0], mx[1]), u1 = fmaxf(mx[2], mx[3]);
-        u0 = fmaxf(u0, __shfl_xor_sync(0xffffffffu, u0, 1));
-        u1 = fmaxf(u1, __shfl_xor_sync(0xffffffffu, u1, 1));
-        u0 = fmaxf(u0, __shfl_xor_sync(0xffffffffu, u0, 2));
-        u1 = fmaxf(u1, __shfl_xor_sync(0xffffffffu, u1, 2));
-        const bool grow = fmaxf(st.m[0], u0 * scale_log2) > st.m[0] + 8.0f ||
-                          fmaxf(st.m[1], u1 * scale_log2) > st.m[1] + 8.0f;
-        if (!__any_sync(0xffffffffu, grow)) {
-            st.cov[0] += 32;
-            st.cov[1] += 32;
-            tmem_st16x128_x16(sAddr, s);
-            tmem_st_wait();
-            return;
-        }
-        tmem_ld16x256_x16(sAddr, s); // a reference moves: redo in order
-        tmem_ld_wait();
-    }
     int nv0 = 64, nv1 = 64;
     if (!full) {
         nv0 = nv1 = 0;
@@ -273,6 +213,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
     const bool any_need = __any_sync(0xffffffffu, need_any);
     // p = exp2(s * scale_log2 - m); masked columns hold -inf -> p = 0. A row
     // with nothing valid yet keeps m = -inf: use 0 so -inf * scale - 0 = -inf.
+    const unsigned long long sc2 = pack_f2(scale_log2, scale_log2);
     unsigned long long nm2[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
