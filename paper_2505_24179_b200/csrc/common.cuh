@@ -115,7 +115,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint64_t t0 = global_timer_ns();
     uint32_t spins = 0;
     while (!mbar_try_wait(a, parity)) {
-        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > SALE_B200_WAIT_TIMEOUT_NS) __trap();
+        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > SALE_B200_WAIT_TIMEOUT_NS) {
+#ifdef SALE_B200_DEBUG_WAIT
+            printf("mbar_wait timeout: block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x,
+                   a & 0xFFFFFu, parity);
+#endif
+            __trap();
+        }
     }
 }
 
@@ -162,7 +168,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
     const uint64_t t0 = global_timer_ns();
     uint32_t spins = 0;
     while (!mbar_try_wait_cluster(a, parity)) {
-        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > SALE_B200_WAIT_TIMEOUT_NS) __trap();
+        if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > SALE_B200_WAIT_TIMEOUT_NS) {
+#ifdef SALE_B200_DEBUG_WAIT
+            printf("mbar_wait timeout: block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x,
+                   a & 0xFFFFFu, parity);
+#endif
+            __trap();
+        }
     }
 }
 
