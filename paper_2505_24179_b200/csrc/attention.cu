@@ -106,6 +106,19 @@ __device__ __forceinline__ uint32_t shl23_add(uint32_t t, uint32_t p) {
     return r;
 }
 
+// 16-byte read-only load / 4-byte store with an L2 cache-policy hint
+__device__ __forceinline__ uint4 ld_stream16(const uint4 *p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st_stream4(void *p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&p);
@@ -490,6 +503,9 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         if (elect_one() && ntiles > 0) {
             tma_prefetch(&tm_k);
             tma_prefetch(&tm_v);
+            // K / V of a KV head are re-read by every query block of its group:
+            // keep them in L2 (Q and O stream through with evict_first)
+            const uint64_t keep = policy_evict_last();
             // K_jj is released by S_jj, V_jj by PV_jj (one tile later): K runs
             // one tile ahead of V so a late PV never holds back the next K.
             auto key0_of = [&](int jj) {
@@ -502,8 +518,8 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                     const int key0 = key0_of(jj);
                     mbar_wait(&sm.k_empty[st], ((jj / kKvStages) & 1) ^ 1);
                     mbar_expect_tx(&sm.k_full[st], 2 * kTileBytesHalf);
-                    tma_load_4d(sm.k[st][0], &tm_k, &sm.k_full[st], 0, g, key0, b);
-                    tma_load_4d(sm.k[st][1], &tm_k, &sm.k_full[st], 64, g, key0, b);
+                    tma_load_4d_hint(sm.k[st][0], &tm_k, &sm.k_full[st], 0, g, key0, b, keep);
+                    tma_load_4d_hint(sm.k[st][1], &tm_k, &sm.k_full[st], 64, g, key0, b, keep);
                 }
                 if (jj > 0) {
                     const int vj = jj - 1;
@@ -511,8 +527,8 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                     const int key0 = key0_of(vj);
                     mbar_wait(&sm.v_empty[st], ((vj / kVStages) & 1) ^ 1);
                     mbar_expect_tx(&sm.v_full[st], 2 * kTileBytesHalf);
-                    tma_load_4d(sm.v[0][st], &tm_v, &sm.v_full[st], 0, g, key0, b);
-                    tma_load_4d(sm.v[1][st], &tm_v, &sm.v_full[st], 64, g, key0, b);
+                    tma_load_4d_hint(sm.v[0][st], &tm_v, &sm.v_full[st], 0, g, key0, b, keep);
+                    tma_load_4d_hint(sm.v[1][st], &tm_v, &sm.v_full[st], 64, g, key0, b, keep);
                 }
             }
             // drain: the last releases of every ring stage (S / PV commits) land
@@ -605,6 +621,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         // head only keeps one softmax warp busy on every SMSP.
         const int wg = (warp - 3) >> 2;          // second index of the warp in its quadrant
         const int quad = warp & 3;               // TMEM lane quadrant (warp id % 4)
+        const uint64_t stream_pol = policy_evict_first();
         // Q staging: thread = TMEM lane 32 quad + lane, column half wg
         {
             const int hh = lane >> 4;
@@ -616,7 +633,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                 q + ((static_cast<int64_t>(b) * tokens + qrow) * hq + hA + hh) * kHeadDim + 64 * wg);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const uint4 w = q_ok ? __ldg(src + e) : make_uint4(0, 0, 0, 0);
+                const uint4 w = q_ok ? ld_stream16(src + e, stream_pol) : make_uint4(0, 0, 0, 0);
                 a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
             }
             tmem_st32(lane_addr + kColQ + 32 * wg, a);
@@ -715,11 +732,13 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             for (int R = 0; R < 8; ++R) {
                 const int col = 64 * cc + 8 * R + 2 * q4;
                 if (ok0)
-                    *reinterpret_cast<uint32_t *>(dst0 + col) =
-                        pack_bf16x2(__uint_as_float(o[4 * R]) * inv0, __uint_as_float(o[4 * R + 1]) * inv0);
+                    st_stream4(dst0 + col,
+                               pack_bf16x2(__uint_as_float(o[4 * R]) * inv0, __uint_as_float(o[4 * R + 1]) * inv0),
+                               stream_pol);
                 if (ok1)
-                    *reinterpret_cast<uint32_t *>(dst1 + col) =
-                        pack_bf16x2(__uint_as_float(o[4 * R + 2]) * inv1, __uint_as_float(o[4 * R + 3]) * inv1);
+                    st_stream4(dst1 + col,
+                               pack_bf16x2(__uint_as_float(o[4 * R + 2]) * inv1, __uint_as_float(o[4 * R + 3]) * inv1),
+                               stream_pol);
             }
         }
         if (q4 == 0 && coverage) {
