@@ -69,6 +69,20 @@ def workload_name(a, tokens=None):
             f"(seed {a.seed}), tau={a.tau}")
 
 
+def bench_config(a, N, B, world):
+    """The config dict of a bench line; both arms print the same one for the
+    same command (the driver compares them)."""
+    Hq, Hkv, d = MODEL["q_heads"], MODEL["kv_heads"], MODEL["head_dim"]
+    split = world // Hkv if world > Hkv and world % Hkv == 0 else 1
+    return {"workload": workload_name(a), "tokens": N, "batch": B, "tau": a.tau,
+            "q_heads": Hq, "kv_heads": Hkv, "head_dim": d,
+            "parallelism": (f"kv-group sharded x{world}, no collective" if split == 1 else
+                            f"{Hkv} kv groups x {split} query-block ranges (K/V "
+                            "replicated), no collective"),
+            "l2": f"inputs ({B * N * (Hq + 2 * Hkv) * d * 2 / 2**30:.2f} GiB) larger "
+                  "than L2; no flush"}
+
+
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full
     capture summary (profiles/ncu_traffic.json), or None."""
@@ -240,7 +254,7 @@ def run_reference(a):
             "data": "synthetic", "impl": "reference",
             "value_is": f"extrapolated to {a.tokens} tokens from measured samples; ms_per_step is "
                         "the measured wall of one step (both samples)",
-            "config": {"workload": workload_name(a), "tokens": a.tokens, "tau": a.tau},
+            "config": bench_config(a, a.tokens, a.batch, world),
             "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": "reference",
                              "sample": sample, "extrapolated": True},
             "c1_measured": {"tokens": sizes[0], "q_heads": MODEL["q_heads"],
@@ -557,13 +571,7 @@ def run_b200(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16 (attention) / int8 (estimator)", "data": "synthetic",
-            "config": {"workload": workload_name(a), "tokens": N, "batch": B, "tau": a.tau,
-                       "q_heads": Hq, "kv_heads": Hkv, "head_dim": d,
-                       "parallelism": (f"kv-group sharded x{world}, no collective" if split == 1 else
-                                       f"{Hkv} kv groups x {split} query-block ranges (K/V "
-                                       "replicated), no collective"),
-                       "l2": f"inputs ({B * N * (Hq + 2 * Hkv) * d * 2 / 2**30:.2f} GiB) larger "
-                             "than L2; no flush"},
+            "config": bench_config(a, N, B, world),
             "speedup_vs_dense": ms_dense / ms_step, "dense_ms": ms_dense,
             "estimation_overhead_pct": 100.0 * overhead, "density": density,
             "stage_ms": stage_ms, "effective_tflops": dense_flops / (ms_step * 1e-3) / 1e12,
