@@ -174,11 +174,20 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
         tmem_st_wait();
         return;
     }
-    tmem_ld16x256_x16(sAddr, s);
-    tmem_ld_wait();
     const bool full = nib == 0xFu && lim0 >= 127 && lim1 >= 127;
     const unsigned long long sc2 = pack_f2(scale_log2, scale_log2);
-    if (__all_sync(0xffffffffu, full && st.m[0] != -INFINITY && st.m[1] != -INFINITY)) {
+    const bool spec = __all_sync(0xffffffffu, full && st.m[0] != -INFINITY && st.m[1] != -INFINITY);
+    if (spec) {
+        // S in two 64-column halves: the second half lands while the first
+        // half's exps run
+        tmem_ld16x256_x8(sAddr, s);
+        tmem_ld_wait();
+        tmem_ld16x256_x8(sAddr + 64, s + 32);
+    } else {
+        tmem_ld16x256_x16(sAddr, s);
+        tmem_ld_wait();
+    }
+    if (spec) {
         // Speculative path (full tiles once both rows have a reference): P is
         // computed against the running references right away, interleaved
         // with the row max instead of after it; when no row max grows by > 8
@@ -191,6 +200,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t sAddr, uint32_t oAddr, uin
         for (int R = 0; R < 16; ++R)
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
+                if (R == 8 && k == 0) tmem_ld_wait(); // the second half
                 mx[2 * k + (R & 1)] =
                     fmax3(mx[2 * k + (R & 1)], __uint_as_float(s[4 * R + 2 * k]), __uint_as_float(s[4 * R + 2 * k + 1]));
                 unsigned long long x =
