@@ -38,8 +38,9 @@
 //           [0, 16) (head 2p + w), two rows x 64 columns per thread through
 //           16x256b loads; row max by two shuffles (no cross-warp barrier);
 //           lazy-rescaled online softmax in the exp2 domain (O | l rescaled in
-//           TMEM only when the running max grows by > 8); P -> bf16 ->
-//           tcgen05.st over S.
+//           TMEM only when the running max grows by > 8); full tiles compute
+//           P speculatively against the running references (redone in order
+//           when a reference moves); P -> bf16 -> tcgen05.st over S.
 #include "common.cuh"
 #include "internal.h"
 
