@@ -508,6 +508,13 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         atomicAdd(&g_attn_prof[9], static_cast<unsigned long long>(clock64() - t_kernel));
     const uint32_t tmem = sm.tmem_base;
     const int ntiles = sm.ntiles;
+    // Alternate groups of 64 query blocks (about one wave of CTAs) walk their
+    // key tiles in opposite directions, so a wave starts on the K / V tiles the
+    // previous wave touched last (still in L2) instead of re-streaming the
+    // head's K / V prefix from HBM. A function of i alone: range and chunked
+    // launches compute every query block exactly as the one-shot launch.
+    const bool rev = ((i >> 6) & 1) != 0;
+    auto tile_at = [&](int jj) -> uint32_t { return sm.tiles[rev ? ntiles - 1 - jj : jj]; };
 
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA
@@ -520,7 +527,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             // K_jj is released by S_jj, V_jj by PV_jj (one tile later): K runs
             // one tile ahead of V so a late PV never holds back the next K.
             auto key0_of = [&](int jj) {
-                const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
+                const int j = static_cast<int>(tile_at(jj) & 0xFFFFu);
                 return j == 0 ? 0 : kBlockK + 128 * (j - 1);
             };
             for (int jj = 0; jj <= ntiles; ++jj) {
@@ -565,7 +572,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
             auto issue_s = [&](int jj) {
                 const int st = jj % kKvStages;
                 const int sb = jj & 1;
-                const int j = static_cast<int>(sm.tiles[jj] & 0xFFFFu);
+                const int j = static_cast<int>(tile_at(jj) & 0xFFFFu);
                 const uint32_t idesc_s = j == 0 ? idesc_bf16(128, 32, false) : idesc_bf16(128, 128, false);
                 const uint64_t kd0 = umma_desc_sw128(smem_u32(sm.k[st][0]), 16, 1024);
                 const uint64_t kd1 = umma_desc_sw128(smem_u32(sm.k[st][1]), 16, 1024);
@@ -595,7 +602,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                 const int nx = pj + 2;
                 const int pst = pj % kVStages;
                 const int psb = pj & 1;
-                const int jp = static_cast<int>(sm.tiles[pj] & 0xFFFFu);
+                const int jp = static_cast<int>(tile_at(pj) & 0xFFFFu);
                 const int steps = jp == 0 ? 2 : 8;
                 if (nx < ntiles) wait_k(nx);
                 if (prof) t0 = clock64();
@@ -671,7 +678,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         long long w_s = 0, t_part = 0, t1 = 0, w_chain = 0, n_chain = 0;
         for (int jj = 0; jj < ntiles; ++jj) {
             const int sb = jj & 1;
-            const uint32_t info = sm.tiles[jj];
+            const uint32_t info = tile_at(jj);
             const int j = static_cast<int>(info & 0xFFFFu);
             const uint32_t nib = (info >> (16 + 4 * half)) & 0xFu;
             const int64_t key0 = j == 0 ? 0 : kBlockK + 128LL * (j - 1);
