@@ -370,7 +370,7 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
                         const __grid_constant__ CUtensorMap tm_v, const uint32_t *__restrict__ mask,
                         __nv_bfloat16 *__restrict__ out, int32_t *__restrict__ coverage,
                         unsigned long long *__restrict__ empty_rows, int64_t tokens, int hq, int hkv,
-                        float scale_log2, int64_t i_lo, int64_t ni) {
+                        float scale_log2, int64_t i_lo, int64_t ni, int wave_qb) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const long long t_kernel = clock64();
     AttnSmem &sm = *reinterpret_cast<AttnSmem *>(smem_raw + smem_pad_1k(smem_raw));
@@ -508,12 +508,13 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         atomicAdd(&g_attn_prof[9], static_cast<unsigned long long>(clock64() - t_kernel));
     const uint32_t tmem = sm.tmem_base;
     const int ntiles = sm.ntiles;
-    // Alternate groups of 64 query blocks (about one wave of CTAs) walk their
+    // Alternate groups of wave_qb query blocks (one wave of CTAs: SMs / head
+    // pairs, counted from the heaviest block, the first to launch) walk their
     // key tiles in opposite directions, so a wave starts on the K / V tiles the
     // previous wave touched last (still in L2) instead of re-streaming the
     // head's K / V prefix from HBM. A function of i alone: range and chunked
     // launches compute every query block exactly as the one-shot launch.
-    const bool rev = ((i >> 6) & 1) != 0;
+    const bool rev = (((nq - 1 - i) / wave_qb) & 1) != 0;
     auto tile_at = [&](int jj) -> uint32_t { return sm.tiles[rev ? ntiles - 1 - jj : jj]; };
 
     if (warp == 0) {
@@ -810,12 +811,15 @@ cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, cons
     if (i_hi < 0 || i_hi > nq) i_hi = nq;
     if (i_hi <= i_lo) return cudaSuccess;
     const int64_t grid = batch * hkv * npairs * (i_hi - i_lo);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int wave_qb = std::max(1, sms / npairs); // query blocks of one wave of CTAs
     auto kern = g_attn_prof_host ? sparse_attention_kernel<true> : sparse_attention_kernel<false>;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
     if (e != cudaSuccess) return e;
     kern<<<static_cast<unsigned>(grid), kAttnThreads, smem, stream>>>(
         static_cast<const __nv_bfloat16 *>(q), tm_k, tm_v, mask, static_cast<__nv_bfloat16 *>(out),
-        coverage, empty_rows, tokens, hq, hkv, scale_log2, i_lo, i_hi - i_lo);
+        coverage, empty_rows, tokens, hq, hkv, scale_log2, i_lo, i_hi - i_lo, wave_qb);
     return cudaGetLastError();
 }
 
