@@ -41,6 +41,8 @@
 //           TMEM only when the running max grows by > 8); full tiles compute
 //           P speculatively against the running references (redone in order
 //           when a reference moves); P -> bf16 -> tcgen05.st over S.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -813,7 +815,14 @@ cudaError_t launch_sparse_attention(const void *q, const CUtensorMap &tm_k, cons
     const int64_t grid = batch * hkv * npairs * (i_hi - i_lo);
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int wave_qb = std::max(1, sms / npairs); // query blocks of one wave of CTAs
+    int wave_qb = std::max(1, sms / npairs); // query blocks of one wave of CTAs
+    // tests: SALE_B200_K3_WAVE_QB overrides the group size, so short sequences
+    // also run the reversed-direction CTAs
+    static const int wave_env = [] {
+        const char *e = getenv("SALE_B200_K3_WAVE_QB");
+        return e ? atoi(e) : 0;
+    }();
+    if (wave_env > 0) wave_qb = wave_env;
     auto kern = g_attn_prof_host ? sparse_attention_kernel<true> : sparse_attention_kernel<false>;
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
     if (e != cudaSuccess) return e;
