@@ -421,6 +421,24 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         }
         fence_barrier_init();
     }
+    // Q of the softmax warps' TMEM lanes: the global loads are issued before the
+    // tile-list build (their latency overlaps it), the TMEM store follows the
+    // CTA barrier (TMEM is allocated by then). Thread = TMEM lane 32 quad +
+    // lane, column half wg.
+    uint32_t qa[32];
+    if (warp >= 3) {
+        const uint64_t pol = policy_evict_first();
+        const int wg = (warp - 3) >> 2, quad = warp & 3, hh = lane >> 4;
+        const int64_t qrow = q0 + quad * 16 + (lane & 15);
+        const bool q_ok = qrow < tokens && (hh == 0 || hasB);
+        const uint4 *src = reinterpret_cast<const uint4 *>(
+            q + ((static_cast<int64_t>(b) * tokens + (q_ok ? qrow : 0)) * hq + hA + hh) * kHeadDim + 64 * wg);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint4 w = q_ok ? ld_stream16(src + e, pol) : make_uint4(0, 0, 0, 0);
+            qa[4 * e] = w.x, qa[4 * e + 1] = w.y, qa[4 * e + 2] = w.z, qa[4 * e + 3] = w.w;
+        }
+    }
     if (warp == 2) {
         tmem_alloc<512>(&sm.tmem_base);
         if (lane == 0 && kProf)
@@ -643,21 +661,10 @@ sparse_attention_kernel(const __nv_bfloat16 *__restrict__ q, const __grid_consta
         const int wg = (warp - 3) >> 2;          // second index of the warp in its quadrant
         const int quad = warp & 3;               // TMEM lane quadrant (warp id % 4)
         const uint64_t stream_pol = policy_evict_first();
-        // Q staging: thread = TMEM lane 32 quad + lane, column half wg
+        // Q staging: the rows loaded before the tile list, into TMEM
         {
-            const int hh = lane >> 4;
-            const int64_t qrow = q0 + quad * 16 + (lane & 15);
-            const bool q_ok = qrow < tokens && (hh == 0 || hasB);
             const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-            uint32_t a[32];
-            const uint4 *src = reinterpret_cast<const uint4 *>(
-                q + ((static_cast<int64_t>(b) * tokens + qrow) * hq + hA + hh) * kHeadDim + 64 * wg);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint4 w = q_ok ? ld_stream16(src + e, stream_pol) : make_uint4(0, 0, 0, 0);
-                a[4 * e] = w.x, a[4 * e + 1] = w.y, a[4 * e + 2] = w.z, a[4 * e + 3] = w.w;
-            }
-            tmem_st32(lane_addr + kColQ + 32 * wg, a);
+            tmem_st32(lane_addr + kColQ + 32 * wg, qa);
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
