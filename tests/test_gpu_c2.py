@@ -185,15 +185,16 @@ def test_c2_gate_32k_all_heads(torch, model, hq, hkv, tau):
     _report(f"c2_32k_{model}_tau{tau}", rep)
 
 
-def test_c2_extension_128k_four_heads_all_query_blocks(torch):
-    """configs[2] size: masks of every query block, statistics and bounds of
-    four heads (one per KV group quarter) against the oracle."""
+@pytest.mark.parametrize("model,hq,hkv,heads", [("llama", 32, 8, (0, 9, 18, 27)),
+                                                 ("qwen", 28, 4, (0, 9, 17, 26))])
+def test_c2_extension_128k_four_heads_all_query_blocks(torch, model, hq, hkv, heads):
+    """configs[2] / configs[3] size: masks of every query block, statistics and
+    bounds of four heads (spread over the KV groups) against the oracle."""
     N, tau = 131072, 0.004
-    inp = Inputs("sink_local", 7, 1, N, 32, 8)
+    inp = Inputs("sink_local", 7, 1, N, hq, hkv)
     q, k, v = inp.torch()
     nq, nk, nw = sale.grid(N)
-    heads = (0, 9, 18, 27)
-    mask = torch.empty((1, 32, nq, nw), dtype=torch.int32, device="cuda")
+    mask = torch.empty((1, hq, nq, nw), dtype=torch.int32, device="cuda")
     sale.prefill(q, k, v, tau, mask_out=mask)
     cells = sale.unpack_mask(_np(mask), N)
     dbg = {}
@@ -215,4 +216,4 @@ def test_c2_extension_128k_four_heads_all_query_blocks(torch):
     rep = _merge([o["rep"] for o in orc])
     rep.update(tokens=N, heads=list(heads), tau=tau)
     assert rep["near_ties"] == 0 and rep["min_decision_rel"] > 1e-12, rep
-    _report("c3_128k_tau0.004", rep)
+    _report("c3_128k_tau0.004" if model == "llama" else f"c4_128k_{model}_tau0.004", rep)
